@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""AIDW hot-path benchmark.
+
+One step = the whole hot path (S1 kNN + r_obs, S3 allreduce of the R bounds when
+N > 1, S4 alpha, S5 weighting pass) over one batch of queries whose data and
+queries are already resident in HBM.
+
+  N = 1 : C4 -- 1,024,000 data x 1,024,000 queries, k = 10, fp32, uniform, GLOBAL
+          R bounds (BASELINE.json configs[3], the metric's 1M x 1M configuration)
+  N > 1 : weak scaling -- every rank owns 1,024,000 queries of one job of
+          N x 1,024,000 queries (data replicated); GLOBAL bounds joined by one
+          NCCL allreduce(MAX) per step.  At N = 8 the job is C5-sized (8.19M).
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle (the
+"reference arm" of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import datagen  # noqa: E402
+
+ND = 1000 * datagen.K_SIZE
+NQ_PER_GPU = 1000 * datagen.K_SIZE
+K_NN = 10
+SEED = 1004  # C4
+METRIC = "AIDW interpolated points/sec (fp32; 1M data x 1M queries per GPU, k=10, GLOBAL R bounds)"
+SFU_PER_PAIR = 2        # lg2 + ex2 per weighting pair
+MUFU_PER_CLK_SM = 16    # B200 SFU lanes per SM per clock (measured: profiles/)
+FP32_PER_CLK_SM = 128
+KNN_FP32_PER_PAIR = 4
+N_SM = 148
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"sm_max_mhz": 1965.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            p = [s.strip() for s in line.split(",")]
+            if len(p) >= 7:
+                self.rows.append(p)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+
+
+def cpu_oracle_rate(x, y, z, qx, qy, target_s=12.0):
+    """Time the oracle as it stands (all host cores) on a bounded query sample of the
+    workload; returns (points/s, cores, sample description)."""
+    import oracle
+    cores = oracle.num_threads()
+    # calibrate with a small sample, then size the sample for ~target_s seconds
+    n0 = max(cores, 16)
+    t0 = time.perf_counter()
+    _oracle_steps(oracle, x, y, z, qx[:n0], qy[:n0])
+    dt0 = time.perf_counter() - t0
+    n = int(min(len(qx), max(n0, n0 * target_s / max(dt0, 1e-3))))
+    n = max(cores, (n // cores) * cores)
+    t0 = time.perf_counter()
+    _oracle_steps(oracle, x, y, z, qx[:n], qy[:n])
+    dt = time.perf_counter() - t0
+    return n / dt, cores, f"{n} of {len(qx)} queries x all {len(x)} data points, full AIDW (kNN + alpha + Eq. 1), fp64"
+
+
+def _oracle_steps(oracle, x, y, z, qx, qy):
+    re = oracle.r_exp(len(x), oracle.bbox_area(x, y))
+    robs = oracle.knn_f64(x, y, qx, qy, K_NN)
+    rmin, rmax = oracle.r_bounds(robs, re, oracle.GLOBAL)
+    a = oracle.alpha(robs, re, datagen.ALPHA_LEVELS, rmin, rmax)
+    return oracle.idw(x, y, z, qx, qy, a)
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    x, y, z = datagen.make_data({"nd": ND, "data": "uniform"}, seed=SEED)
+    qx, qy = datagen.uniform_points(SEED, NQ_PER_GPU * args.gpus, datagen.S_QX, datagen.S_QY)
+    import oracle
+    oracle.build()
+    cores = oracle.num_threads()
+    # each step: a bounded sample sized so the whole run ends within minutes
+    per_step = max(cores, int(args.ref_queries_per_step or 4 * cores))
+    times = []
+    for i in range(args.warmup + args.steps):
+        s = (i * per_step) % (len(qx) - per_step)
+        t0 = time.perf_counter()
+        _oracle_steps(oracle, x, y, z, qx[s:s + per_step], qy[s:s + per_step])
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * float(np.mean(times))
+    value = per_step / (ms / 1e3)
+    sample = f"{per_step} queries per step x all {ND} data points, full AIDW (kNN + alpha + Eq. 1), fp64"
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args.gpus), "nd": ND, "k": K_NN},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def workload_name(n):
+    if n == 1:
+        return "C4: 1,024,000 data x 1,024,000 queries, k=10, fp32, uniform, GLOBAL R bounds"
+    return (f"C4 weak-scaled: 1,024,000 data x {n}x1,024,000 queries ({NQ_PER_GPU} per GPU), k=10, fp32, "
+            f"uniform, GLOBAL R bounds allreduced over {n} GPUs")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no baselines, no flush)")
+    ap.add_argument("--nq", type=int, default=NQ_PER_GPU, help="queries per GPU (default C4)")
+    ap.add_argument("--ref-queries-per-step", type=int, default=0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1511_02186_b200 as P
+    from paper_1511_02186_b200.partition import allreduce_bounds
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+
+    nq = args.nq
+    x, y, z = datagen.make_data({"nd": ND, "data": "uniform"}, seed=SEED)
+    qx_np, qy_np = datagen.uniform_points(SEED, nq, datagen.S_QX, datagen.S_QY, offset=rank * nq)
+    eng = P.AIDW(x, y, z, dtype=torch.float32, device=local)
+    qx = torch.as_tensor(qx_np, dtype=torch.float32, device=dev)
+    qy = torch.as_tensor(qy_np, dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream(dev)
+    flush = None if args.profile else torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+
+    r_obs = torch.empty(nq, dtype=torch.float32, device=dev)
+    d1 = torch.empty_like(r_obs)
+    al = torch.empty_like(r_obs)
+    zo = torch.empty_like(r_obs)
+    mm = torch.empty(2, dtype=torch.float32, device=dev)
+    lv = datagen.ALPHA_LEVELS
+
+    def step(ev=None):
+        if ev: ev[0].record(st)
+        P.aidw_knn_robs(eng.h, qx, qy, K_NN, r_obs, d1, mm, None, st)
+        if ev: ev[1].record(st)
+        if group is not None:
+            allreduce_bounds(mm, group)
+        if ev: ev[2].record(st)
+        P.aidw_alpha(eng.h, r_obs, lv, P.GLOBAL, 0.0, 0.0, mm, P.NORMALIZED, al, st)
+        if ev: ev[3].record(st)
+        P.aidw_interpolate(eng.h, qx, qy, al, d1, zo, st)
+        if ev: ev[4].record(st)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if args.profile:
+        step()
+        torch.cuda.synchronize()
+        if rank == 0:
+            print(json.dumps({"profile_run": True, "nq": nq}))
+        return 0
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    launches0 = eng.launches
+    if group is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)  # L2 flush (256 MiB write) outside the step's events
+            step(evs[i])
+        torch.cuda.synchronize()
+    if group is not None:
+        dist.barrier()
+    launches = eng.launches - launches0
+    per = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(4)] for i in range(args.steps)])
+    step_ms = per.sum(1)
+    ms_local = float(step_ms.mean())
+    if group is not None:
+        t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    else:
+        ms = ms_local
+    zs = zo[:8].cpu()
+    assert torch.isfinite(zs).all()
+
+    # ---- e2e: public API from pinned host buffers, H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.as_tensor(qx_np, dtype=torch.float32).pin_memory()
+        hy = torch.as_tensor(qy_np, dtype=torch.float32).pin_memory()
+        hz = torch.empty(nq, dtype=torch.float32).pin_memory()
+        e2e_steps = max(1, min(args.steps, 3))
+        if group is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        tot = 0.0
+        for i in range(e2e_steps):
+            flush.fill_(i & 0xFF)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            if group is None:
+                eng.run_host(hx, hy, K_NN, lv, P.GLOBAL, out=hz)  # C ABI aidw_run_host
+            else:
+                dx = hx.to(dev, non_blocking=True)
+                dy = hy.to(dev, non_blocking=True)
+                zz = eng.run(dx, dy, K_NN, lv, P.GLOBAL, group=group)
+                hz.copy_(zz, non_blocking=True)
+            e1.record(st)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        e2e_ms = tot / e2e_steps
+        if group is not None:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": nq * world / (e2e_ms / 1e3), "unit": "points/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 2 * 4 * nq * world, "d2h_bytes_per_step": 4 * nq * world,
+               "api": "aidw_run_host (C ABI, pinned host buffers)" if group is None else
+                      "AIDW.run + torch H2D/D2H (pinned), NCCL allreduce"}
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+
+    pk = peaks()
+    clocks = clk.summary()
+    f_max = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
+    pairs = float(nq) * ND
+    knn_ms = float(per[:, 0].mean())
+    ar_ms = float(per[:, 1].mean())
+    alpha_ms = float(per[:, 2].mean())
+    interp_ms = float(per[:, 3].mean())
+    # dominant kernel: the weighting pass, SFU-bound (2 MUFU per pair)
+    interp_rate = pairs / (interp_ms / 1e3)
+    sfu_peak_pairs = N_SM * MUFU_PER_CLK_SM / SFU_PER_PAIR * f_max
+    path_clk_per_pair = (KNN_FP32_PER_PAIR / FP32_PER_CLK_SM + SFU_PER_PAIR / MUFU_PER_CLK_SM) / 1.0
+    path_peak_pairs = N_SM * f_max / path_clk_per_pair
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic = tr.get("interp_dram_bytes_per_launch")
+    except Exception:
+        pass
+    value = nq * world / (ms / 1e3)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        rate, cores, sample = cpu_oracle_rate(x, y, z, qx_np, qy_np)
+        cpu = {"value": rate, "unit": "points/s", "cores": cores, "kind": "oracle", "sample": sample}
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "points/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": workload_name(world), "nd": ND, "nq_per_gpu": nq, "nq_total": nq * world,
+                   "k": K_NN, "alpha_levels": list(lv), "rbounds": "global", "mu": "normalized",
+                   "l2": "flushed between steps (256 MiB write outside the timed events)",
+                   "parallelism": f"query-sharded x{world}, data replicated"},
+        "pair_evals_per_s": 2 * pairs * world / (ms / 1e3),
+        "aidw_pairs_per_s": pairs * world / (ms / 1e3),
+        "phases_ms": {"knn_robs": knn_ms, "allreduce": ar_ms, "alpha": alpha_ms, "interpolate": interp_ms},
+        "roofline": {
+            "bound": "alu", "kernel": "interp_kernel (S5 weighting pass)",
+            "achieved": interp_rate / 1e9, "peak": sfu_peak_pairs / 1e9, "unit": "Gpair/s",
+            "frac": interp_rate / sfu_peak_pairs, "traffic": traffic,
+            "peak_basis": f"{N_SM} SM x {MUFU_PER_CLK_SM} MUFU/clk / {SFU_PER_PAIR} MUFU per pair x "
+                          f"{f_max / 1e6:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
+            "path_frac": (pairs / (ms / 1e3)) / path_peak_pairs,
+            "path_peak_basis": "kNN 4 FP32/pair @128/clk + weighting 2 MUFU/pair @16/clk, per SM",
+            "frac_at_measured_clock": (interp_rate / sfu_peak_pairs) * (f_max / (clocks["sm_mhz"] * 1e6))
+            if clocks.get("sm_mhz") else None,
+        },
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    print(json.dumps(out), flush=True)
+    if group is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,194 @@
+/*
+ * aidw.h -- C ABI of the B200 AIDW hot path (arXiv 1511.02186, "GPU-accelerated
+ * Adaptive IDW").  Implemented by paper_1511_02186_b200/libaidw.so (sm_100a).
+ *
+ * The path:
+ *   aidw_create       S0  repack data to internal SoA, bbox area A, r_exp (Eq. 2)
+ *   aidw_knn_robs     S1-S2  brute-force kNN per query (§3.1.2), r_obs (Eq. 3),
+ *                          nearest squared distance, local {-min, max} of r_obs
+ *   (caller)          S3  GLOBAL mode: allreduce(MAX) of {-min, max} across ranks
+ *   aidw_alpha        S4  R (Eq. 4), mu_R (Eq. 5), alpha (Eq. 6)
+ *   aidw_interpolate  S5  Shepard weighted average over ALL data points (Eq. 1)
+ *   aidw_destroy
+ *
+ * Conventions (all entry points):
+ *  - Every pointer argument documented "device" must be device memory of the
+ *    handle's device (e.g. a torch CUDA tensor's data_ptr()).  The caller owns it
+ *    and keeps it alive until `stream` has passed the call.
+ *  - "T" below is the handle's dtype: float for AIDW_F32, double for AIDW_F64
+ *    (the paper's REAL).  Arrays are dense, 1-D, contiguous.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    asynchronous on it, except aidw_create, aidw_check and aidw_run_host, which
+ *    synchronise it.
+ *  - Argument errors are returned synchronously and nothing is enqueued.
+ *    Per-query data errors (non-finite query coordinates) set a device flag
+ *    holding the smallest failing query index; aidw_check() reports it
+ *    (batch all-or-nothing).
+ *  - No exceptions cross the ABI.  A handle is not thread-safe: use one handle
+ *    per (device, stream) at a time.
+ *  - nq == 0 is a successful no-op.  k must be in [1, 32], nd >= k.
+ */
+#ifndef AIDW_H
+#define AIDW_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define AIDW_API __attribute__((visibility("default")))
+#else
+#define AIDW_API
+#endif
+
+#define AIDW_ABI_VERSION 1
+#define AIDW_KMAX 32
+
+typedef struct aidw_ctx *aidw_t;
+
+typedef enum {
+    AIDW_OK = 0,
+    AIDW_E_INVALID_ARG = 1,        /* null/negative/misaligned argument, bad enum, bad levels */
+    AIDW_E_INSUFFICIENT_DATA = 2,  /* nd < k */
+    AIDW_E_DEGENERATE_EXTENT = 3,  /* bbox area A == 0 */
+    AIDW_E_INVALID_AREA = 4,       /* explicit area < 0 or non-finite */
+    AIDW_E_INVALID_BOUNDS = 5,     /* FIXED r_min >= r_max */
+    AIDW_E_NONFINITE_INPUT = 6,    /* NaN/Inf in data or query coordinates */
+    AIDW_E_UNSUPPORTED = 7,        /* k > AIDW_KMAX, unknown dtype/layout */
+    AIDW_E_CUDA = 8,               /* a CUDA runtime error (message in aidw_last_error) */
+    AIDW_E_NOMEM = 9
+} aidw_status;
+
+/* REAL = float | double. */
+typedef enum { AIDW_F32 = 0, AIDW_F64 = 1 } aidw_dtype;
+
+/* Input layouts accepted at the boundary (Fig. 2).  Internally
+ * the data is always repacked to SoA.
+ *   SOA : x[nd], y[nd], z[nd] back to back
+ *   AOS : (x, y, z) records, 3*nd values
+ *   AOAS: (x, y, z, pad) records, 4*nd values (Array of aligned Structures) */
+typedef enum { AIDW_SOA = 0, AIDW_AOS = 1, AIDW_AOAS = 2 } aidw_layout;
+
+/* Source of R_min / R_max in Eq. 5 (reading R7).
+ *   GLOBAL: min / max of R over all queries of the job (north star; across ranks
+ *           after an allreduce(MAX) of {-min r_obs, max r_obs})
+ *   FIXED : caller-given bounds; the paper's default is 0.0 / 2.0 */
+typedef enum { AIDW_RB_GLOBAL = 0, AIDW_RB_FIXED = 1 } aidw_rbounds;
+
+/* Argument of the cosine in Eq. 5 (reading R8).
+ *   NORMALIZED: pi (R - Rmin) / (Rmax - Rmin)      (default; mu(Rmax) = 1)
+ *   PRINTED   : pi / Rmax * (R - Rmin)             (as typeset) */
+typedef enum { AIDW_MU_NORMALIZED = 0, AIDW_MU_PRINTED = 1 } aidw_muform;
+
+AIDW_API int aidw_abi_version(void);
+AIDW_API const char *aidw_status_string(aidw_status s);
+
+/* Last error message of handle h (or of the calling thread's last failed
+ * aidw_create when h == NULL).  Valid until the next call on that handle. */
+AIDW_API const char *aidw_last_error(aidw_t h);
+
+/*
+ * aidw_create -- S0.  Copy the nd data points (x_i, y_i, z_i) -- the paper's
+ * dx, dy, dz; z is the VALUE, geometry is 2-D -- into a
+ * handle-owned SoA layout padded to the tile multiple, compute the study area
+ * A and r_exp = 1 / (2 sqrt(nd / A)) (Eq. 2) in fp64.
+ *   out      : receives the handle
+ *   device   : CUDA device ordinal
+ *   dt, lay  : dtype of data_xyz and its layout (see aidw_layout)
+ *   data_xyz : device OR host pointer to the data in layout `lay`, dtype `dt`;
+ *              may be freed once aidw_create returns
+ *   nd       : number of data points, >= 1
+ *   area     : > 0 explicit A; == 0 -> A = area of the data's axis-aligned bbox
+ *              (R5); < 0 or non-finite -> AIDW_E_INVALID_AREA
+ * Synchronises `stream` once (A == 0 must be reported synchronously:
+ * AIDW_E_DEGENERATE_EXTENT).  Non-finite data -> AIDW_E_NONFINITE_INPUT.
+ */
+AIDW_API aidw_status aidw_create(aidw_t *out, int device, aidw_dtype dt, aidw_layout lay,
+                        const void *data_xyz, int64_t nd, double area, void *stream);
+
+/* Properties of a handle (host values). */
+AIDW_API int64_t aidw_nd(aidw_t h);
+AIDW_API double aidw_area(aidw_t h);
+AIDW_API double aidw_r_exp(aidw_t h);
+AIDW_API aidw_dtype aidw_dtype_of(aidw_t h);
+
+/*
+ * aidw_knn_robs -- S1 + S2.  For each query S0 = (qx[q], qy[q]), the k smallest
+ * distances to ALL nd data points (brute force, §3.1.2 Steps 1-3,
+ * PAPER.md:317-340; strict "<" as in Step 3) and r_obs = (1/k) sum_i d_i
+ * (Eq. 3), summed in ascending order.
+ * Distance arithmetic (R16), in T with round-to-nearest:
+ *   dx = qx - px; dy = qy - py; s = fma(dx, dx, dy*dy); selection on s; d = sqrt(s).
+ *   qx, qy      : device T[nq]
+ *   k           : 1..AIDW_KMAX, nd >= k (else AIDW_E_INSUFFICIENT_DATA)
+ *   r_obs       : device T[nq] out
+ *   d1sq        : device T[nq] out, nullable: s of the nearest data point (used by
+ *                 aidw_interpolate to scale weights and detect coincidence)
+ *   robs_minmax : device T[2] out, nullable: {-min_q r_obs, max_q r_obs} over these
+ *                 nq queries, ready for an allreduce(MAX); nq == 0 writes {-inf, -inf}
+ *   knn_dists   : device T[nq*k] out, nullable: the k distances per query, ascending
+ *                 (verification output of the same kernel)
+ */
+AIDW_API aidw_status aidw_knn_robs(aidw_t h, const void *qx, const void *qy, int64_t nq, int k,
+                          void *r_obs, void *d1sq, void *robs_minmax, void *knn_dists,
+                          void *stream);
+
+/*
+ * aidw_alpha -- S4.  Per query, in fp64: R = r_obs / r_exp (Eq. 4);
+ * mu_R by Eq. 5 (`mf` selects the cosine argument; intervals
+ * resolve first-match in printed order, R_max == R_min gives mu = 0); alpha by
+ * Eq. 6 (first match in printed order).  alpha is rounded to T.
+ *   r_obs       : device T[nq] (from aidw_knn_robs)
+ *   alpha_lv    : HOST double[5], alpha_1..alpha_5, finite and > 0
+ *   rb          : GLOBAL -> bounds from robs_minmax (device T[2] = {-min r_obs, max r_obs},
+ *                 divided by r_exp); FIXED -> r_min < r_max (else AIDW_E_INVALID_BOUNDS)
+ *   alpha       : device T[nq] out
+ */
+AIDW_API aidw_status aidw_alpha(aidw_t h, const void *r_obs, int64_t nq, const double *alpha_lv,
+                       aidw_rbounds rb, double r_min, double r_max,
+                       const void *robs_minmax, aidw_muform mf, void *alpha, void *stream);
+
+/*
+ * aidw_interpolate -- S5.  Z(S0) = sum_i w_i z_i / sum_i w_i over ALL nd data points,
+ * w_i = d_i^-alpha (Eq. 1; all points).
+ * Evaluated as w_i = 2^(-alpha/2 * log2(s_i / d1sq)) (scaled by the nearest
+ * distance, which cancels in Eq. 1).  fp32: MUFU lg2/ex2, sums in fp32 within
+ * 512-point tiles and fp64 across tiles; fp64: libdevice log2/exp2, fp64 sums.
+ * Exact coincidence (d1sq == 0): Z = mean of z over the data points at distance 0
+ * (R19).
+ *   qx, qy : device T[nq];  alpha : device T[nq] (from aidw_alpha)
+ *   d1sq   : device T[nq] from aidw_knn_robs, or NULL: computed internally (k = 1 pass)
+ *   z_out  : device T[nq] out
+ */
+AIDW_API aidw_status aidw_interpolate(aidw_t h, const void *qx, const void *qy, int64_t nq,
+                             const void *alpha, const void *d1sq, void *z_out, void *stream);
+
+/*
+ * aidw_run_host -- the whole single-GPU path from HOST buffers: H2D of the
+ * queries, knn_robs, (GLOBAL: local bounds = the job's bounds), alpha,
+ * interpolate, D2H of Z; synchronises `stream` and reports deferred errors.
+ *   qx_host, qy_host : host T[nq] (pinned memory gives asynchronous copies)
+ *   z_host           : host T[nq] out
+ * Other arguments as in aidw_knn_robs / aidw_alpha.  Device scratch is owned by
+ * the handle and reused across calls.
+ */
+AIDW_API aidw_status aidw_run_host(aidw_t h, const void *qx_host, const void *qy_host, int64_t nq,
+                          int k, const double *alpha_lv, aidw_rbounds rb, double r_min,
+                          double r_max, aidw_muform mf, void *z_host, void *stream);
+
+/* Synchronise `stream`, then report (and clear) deferred per-query errors:
+ * AIDW_E_NONFINITE_INPUT with the first failing query index in aidw_last_error. */
+AIDW_API aidw_status aidw_check(aidw_t h, void *stream);
+
+/* Number of kernels the handle has launched since creation (launch accounting). */
+AIDW_API int64_t aidw_launch_count(aidw_t h);
+
+AIDW_API aidw_status aidw_destroy(aidw_t h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AIDW_H */

@@ -1,0 +1,368 @@
+// aidw_api.cu -- the C ABI declared in include/aidw.h: argument validation,
+// handle ownership, dispatch to the sm_100a kernels, status codes.
+#include "aidw.h"
+#include "aidw_internal.h"
+
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+struct aidw_ctx {
+    int device = 0;
+    aidw_dtype dt = AIDW_F32;
+    int64_t nd = 0, ndp = 0;
+    double area = 0.0, r_exp = 0.0;
+    void *data = nullptr;            // [3][ndp] T, internal SoA
+    aidw::Scratch *sc = nullptr;     // device scratch
+    void *work = nullptr;            // run_host / internal d1sq scratch
+    size_t work_bytes = 0;
+    int64_t launches = 0;
+    char err[512] = {0};
+};
+
+namespace {
+
+thread_local char g_err[512];
+
+size_t tsize(aidw_dtype dt) { return dt == AIDW_F32 ? sizeof(float) : sizeof(double); }
+
+aidw_status fail(aidw_t h, aidw_status st, const char *fmt, ...)
+{
+    char *buf = h ? h->err : g_err;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, 512, fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+aidw_status cuda_fail(aidw_t h, cudaError_t e, const char *where)
+{
+    return fail(h, AIDW_E_CUDA, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define CK(h, call)                                                       \
+    do {                                                                  \
+        cudaError_t e_ = (call);                                          \
+        if (e_ != cudaSuccess) return cuda_fail((h), e_, #call);          \
+    } while (0)
+
+aidw_status launched(aidw_t h, int n, const char *what)
+{
+    if (n < 0) {
+        cudaError_t e = cudaGetLastError();
+        return cuda_fail(h, e, what);
+    }
+    h->launches += n;
+    return AIDW_OK;
+}
+
+aidw_status ensure_work(aidw_t h, size_t bytes)
+{
+    if (h->work_bytes >= bytes) return AIDW_OK;
+    if (h->work) {
+        cudaDeviceSynchronize();
+        cudaFree(h->work);
+        h->work = nullptr;
+        h->work_bytes = 0;
+    }
+    cudaError_t e = cudaMalloc(&h->work, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(h, AIDW_E_NOMEM, "cudaMalloc(%zu) for scratch: %s", bytes, cudaGetErrorString(e));
+    }
+    h->work_bytes = bytes;
+    return AIDW_OK;
+}
+
+bool is_device_ptr(const void *p)
+{
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+double decode_key(unsigned long long k)
+{
+    unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    double d;
+    std::memcpy(&d, &u, sizeof d);
+    return d;
+}
+
+aidw_status check_levels(aidw_t h, const double *lv)
+{
+    if (!lv) return fail(h, AIDW_E_INVALID_ARG, "alpha_lv is NULL");
+    for (int i = 0; i < 5; ++i)
+        if (!(std::isfinite(lv[i]) && lv[i] > 0.0))
+            return fail(h, AIDW_E_INVALID_ARG, "alpha_lv[%d] = %g must be finite and > 0", i, lv[i]);
+    return AIDW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int aidw_abi_version(void) { return AIDW_ABI_VERSION; }
+
+const char *aidw_status_string(aidw_status s)
+{
+    switch (s) {
+    case AIDW_OK: return "AIDW_OK";
+    case AIDW_E_INVALID_ARG: return "AIDW_E_INVALID_ARG";
+    case AIDW_E_INSUFFICIENT_DATA: return "AIDW_E_INSUFFICIENT_DATA";
+    case AIDW_E_DEGENERATE_EXTENT: return "AIDW_E_DEGENERATE_EXTENT";
+    case AIDW_E_INVALID_AREA: return "AIDW_E_INVALID_AREA";
+    case AIDW_E_INVALID_BOUNDS: return "AIDW_E_INVALID_BOUNDS";
+    case AIDW_E_NONFINITE_INPUT: return "AIDW_E_NONFINITE_INPUT";
+    case AIDW_E_UNSUPPORTED: return "AIDW_E_UNSUPPORTED";
+    case AIDW_E_CUDA: return "AIDW_E_CUDA";
+    case AIDW_E_NOMEM: return "AIDW_E_NOMEM";
+    }
+    return "AIDW_E_UNKNOWN";
+}
+
+const char *aidw_last_error(aidw_t h) { return h ? h->err : g_err; }
+
+aidw_status aidw_create(aidw_t *out, int device, aidw_dtype dt, aidw_layout lay, const void *data_xyz,
+                        int64_t nd, double area, void *stream)
+{
+    if (!out) return fail(nullptr, AIDW_E_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (dt != AIDW_F32 && dt != AIDW_F64) return fail(nullptr, AIDW_E_UNSUPPORTED, "unknown dtype %d", (int)dt);
+    if (lay != AIDW_SOA && lay != AIDW_AOS && lay != AIDW_AOAS)
+        return fail(nullptr, AIDW_E_UNSUPPORTED, "unknown layout %d", (int)lay);
+    if (!data_xyz) return fail(nullptr, AIDW_E_INVALID_ARG, "data_xyz is NULL");
+    if (nd < 1) return fail(nullptr, AIDW_E_INVALID_ARG, "nd = %lld must be >= 1", (long long)nd);
+    if (std::isnan(area) || std::isinf(area) || area < 0.0)
+        return fail(nullptr, AIDW_E_INVALID_AREA, "area = %g must be > 0 (explicit) or 0 (bbox)", area);
+    if (nd > (int64_t)1 << 40) return fail(nullptr, AIDW_E_UNSUPPORTED, "nd too large");
+
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+    aidw_ctx *h = new (std::nothrow) aidw_ctx;
+    if (!h) return fail(nullptr, AIDW_E_NOMEM, "host allocation failed");
+    h->device = device;
+    h->dt = dt;
+    h->nd = nd;
+    h->ndp = (nd + aidw::kPad - 1) / aidw::kPad * aidw::kPad;
+    const size_t ts = tsize(dt);
+    const size_t ncomp = lay == AIDW_AOAS ? 4 : 3;
+    const size_t in_bytes = (size_t)nd * ncomp * ts;
+
+    auto bail = [&](aidw_status s) {
+        std::memcpy(g_err, h->err, sizeof g_err);
+        aidw_destroy(h);
+        return s;
+    };
+
+    if ((e = cudaMalloc(&h->data, 3 * (size_t)h->ndp * ts)) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(h, AIDW_E_NOMEM, "cudaMalloc data: %s", cudaGetErrorString(e)));
+    }
+    if ((e = cudaMalloc(&h->sc, sizeof(aidw::Scratch))) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(h, AIDW_E_NOMEM, "cudaMalloc scratch: %s", cudaGetErrorString(e)));
+    }
+    aidw::Scratch init{};
+    init.mn = ~0ull;
+    init.mx = 0ull;
+    init.done = 0;
+    init.err_idx = LLONG_MAX;
+    init.keys[0] = ~0ull;
+    init.keys[1] = 0ull;
+    init.keys[2] = ~0ull;
+    init.keys[3] = 0ull;
+    init.nonfinite = 0;
+    if ((e = cudaMemcpy(h->sc, &init, sizeof init, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return bail(cuda_fail(h, e, "init scratch"));
+
+    const void *src = data_xyz;
+    void *staged = nullptr;
+    if (!is_device_ptr(data_xyz)) {  // host data: stage it
+        if ((e = cudaMalloc(&staged, in_bytes)) != cudaSuccess) {
+            cudaGetLastError();
+            return bail(fail(h, AIDW_E_NOMEM, "cudaMalloc staging: %s", cudaGetErrorString(e)));
+        }
+        if ((e = cudaMemcpyAsync(staged, data_xyz, in_bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
+            cudaFree(staged);
+            return bail(cuda_fail(h, e, "H2D data"));
+        }
+        src = staged;
+    }
+    aidw_status s = launched(h, aidw::launch_prep((int)dt, (int)lay, src, nd, h->ndp, h->data, h->sc, st),
+                             "prep kernel");
+    aidw::Scratch back;
+    if (s == AIDW_OK) {
+        if ((e = cudaMemcpyAsync(&back, h->sc, sizeof back, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+            (e = cudaStreamSynchronize(st)) != cudaSuccess)
+            s = cuda_fail(h, e, "read bbox");
+    }
+    if (staged) cudaFree(staged);
+    if (s != AIDW_OK) return bail(s);
+    if (back.nonfinite)
+        return bail(fail(h, AIDW_E_NONFINITE_INPUT, "%llu data values are NaN/Inf", back.nonfinite));
+
+    // A: explicit, or the exact bbox (min/max exact; fp64 sub and mul) -- DESIGN.md R5
+    const double x0 = decode_key(back.keys[0]), x1 = decode_key(back.keys[1]);
+    const double y0 = decode_key(back.keys[2]), y1 = decode_key(back.keys[3]);
+    h->area = area > 0.0 ? area : (x1 - x0) * (y1 - y0);
+    if (!(h->area > 0.0) || std::isinf(h->area))
+        return bail(fail(h, AIDW_E_DEGENERATE_EXTENT, "study area A = %g (bbox [%g,%g]x[%g,%g])", h->area, x0,
+                         x1, y0, y1));
+    h->r_exp = 1.0 / (2.0 * std::sqrt((double)nd / h->area));  // Eq. 2, printed order
+    *out = h;
+    return AIDW_OK;
+}
+
+int64_t aidw_nd(aidw_t h) { return h ? h->nd : -1; }
+double aidw_area(aidw_t h) { return h ? h->area : 0.0; }
+double aidw_r_exp(aidw_t h) { return h ? h->r_exp : 0.0; }
+aidw_dtype aidw_dtype_of(aidw_t h) { return h ? h->dt : AIDW_F32; }
+int64_t aidw_launch_count(aidw_t h) { return h ? h->launches : -1; }
+
+aidw_status aidw_knn_robs(aidw_t h, const void *qx, const void *qy, int64_t nq, int k, void *r_obs,
+                          void *d1sq, void *robs_minmax, void *knn_dists, void *stream)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    if (nq < 0) return fail(h, AIDW_E_INVALID_ARG, "nq < 0");
+    if (k < 1) return fail(h, AIDW_E_INVALID_ARG, "k = %d must be >= 1", k);
+    if (k > AIDW_KMAX) return fail(h, AIDW_E_UNSUPPORTED, "k = %d > AIDW_KMAX = %d", k, AIDW_KMAX);
+    if (h->nd < k)
+        return fail(h, AIDW_E_INSUFFICIENT_DATA, "nd = %lld < k = %d", (long long)h->nd, k);
+    if (nq > 0 && (!qx || !qy || !r_obs)) return fail(h, AIDW_E_INVALID_ARG, "qx/qy/r_obs is NULL");
+    if (nq > (int64_t)1 << 40) return fail(h, AIDW_E_UNSUPPORTED, "nq too large");
+    CK(h, cudaSetDevice(h->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (nq == 0) {
+        if (robs_minmax) return launched(h, aidw::launch_minmax_identity((int)h->dt, robs_minmax, st), "minmax");
+        return AIDW_OK;
+    }
+    return launched(h,
+                    aidw::launch_knn((int)h->dt, k, h->data, h->ndp, qx, qy, nq, r_obs, d1sq, robs_minmax,
+                                     knn_dists, h->sc, st),
+                    "knn_robs kernel");
+}
+
+aidw_status aidw_alpha(aidw_t h, const void *r_obs, int64_t nq, const double *alpha_lv, aidw_rbounds rb,
+                       double r_min, double r_max, const void *robs_minmax, aidw_muform mf, void *alpha,
+                       void *stream)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    if (nq < 0) return fail(h, AIDW_E_INVALID_ARG, "nq < 0");
+    aidw_status s = check_levels(h, alpha_lv);
+    if (s != AIDW_OK) return s;
+    if (rb != AIDW_RB_GLOBAL && rb != AIDW_RB_FIXED) return fail(h, AIDW_E_INVALID_ARG, "bad rbounds");
+    if (mf != AIDW_MU_NORMALIZED && mf != AIDW_MU_PRINTED) return fail(h, AIDW_E_INVALID_ARG, "bad muform");
+    if (rb == AIDW_RB_FIXED) {
+        if (!(std::isfinite(r_min) && std::isfinite(r_max)))
+            return fail(h, AIDW_E_INVALID_BOUNDS, "r_min/r_max must be finite");
+        if (!(r_min < r_max)) return fail(h, AIDW_E_INVALID_BOUNDS, "r_min = %g >= r_max = %g", r_min, r_max);
+    } else if (nq > 0 && !robs_minmax) {
+        return fail(h, AIDW_E_INVALID_ARG, "GLOBAL bounds need robs_minmax");
+    }
+    if (nq == 0) return AIDW_OK;
+    if (!r_obs || !alpha) return fail(h, AIDW_E_INVALID_ARG, "r_obs/alpha is NULL");
+    CK(h, cudaSetDevice(h->device));
+    return launched(h,
+                    aidw::launch_alpha((int)h->dt, r_obs, nq, h->r_exp, alpha_lv, (int)rb, r_min, r_max,
+                                       robs_minmax, (int)mf, alpha, static_cast<cudaStream_t>(stream)),
+                    "alpha kernel");
+}
+
+aidw_status aidw_interpolate(aidw_t h, const void *qx, const void *qy, int64_t nq, const void *alpha,
+                             const void *d1sq, void *z_out, void *stream)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    if (nq < 0) return fail(h, AIDW_E_INVALID_ARG, "nq < 0");
+    if (nq == 0) return AIDW_OK;
+    if (!qx || !qy || !alpha || !z_out) return fail(h, AIDW_E_INVALID_ARG, "qx/qy/alpha/z_out is NULL");
+    CK(h, cudaSetDevice(h->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!d1sq) {  // nearest squared distance via the k = 1 kNN pass
+        const size_t ts = tsize(h->dt);
+        aidw_status s = ensure_work(h, 2 * (size_t)nq * ts);
+        if (s != AIDW_OK) return s;
+        void *robs = h->work;
+        void *d1 = static_cast<char *>(h->work) + (size_t)nq * ts;
+        s = launched(h,
+                     aidw::launch_knn((int)h->dt, 1, h->data, h->ndp, qx, qy, nq, robs, d1, nullptr, nullptr,
+                                      h->sc, st),
+                     "nearest kernel");
+        if (s != AIDW_OK) return s;
+        d1sq = d1;
+    }
+    return launched(h, aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, alpha, d1sq, z_out, st),
+                    "interpolate kernel");
+}
+
+aidw_status aidw_check(aidw_t h, void *stream)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    CK(h, cudaSetDevice(h->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CK(h, cudaStreamSynchronize(st));
+    CK(h, cudaGetLastError());
+    long long idx = 0;
+    CK(h, cudaMemcpy(&idx, &h->sc->err_idx, sizeof idx, cudaMemcpyDeviceToHost));
+    if (idx != LLONG_MAX) {
+        const long long none = LLONG_MAX;
+        CK(h, cudaMemcpy(&h->sc->err_idx, &none, sizeof none, cudaMemcpyHostToDevice));
+        return fail(h, AIDW_E_NONFINITE_INPUT, "non-finite query coordinate at query index %lld", idx);
+    }
+    return AIDW_OK;
+}
+
+aidw_status aidw_run_host(aidw_t h, const void *qx_host, const void *qy_host, int64_t nq, int k,
+                          const double *alpha_lv, aidw_rbounds rb, double r_min, double r_max, aidw_muform mf,
+                          void *z_host, void *stream)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    if (nq < 0) return fail(h, AIDW_E_INVALID_ARG, "nq < 0");
+    if (nq == 0) return AIDW_OK;
+    if (!qx_host || !qy_host || !z_host) return fail(h, AIDW_E_INVALID_ARG, "NULL host buffer");
+    aidw_status s = check_levels(h, alpha_lv);
+    if (s != AIDW_OK) return s;
+    if (rb == AIDW_RB_FIXED && !(r_min < r_max))
+        return fail(h, AIDW_E_INVALID_BOUNDS, "r_min = %g >= r_max = %g", r_min, r_max);
+    if (k < 1 || k > AIDW_KMAX) return fail(h, k < 1 ? AIDW_E_INVALID_ARG : AIDW_E_UNSUPPORTED, "k = %d", k);
+    if (h->nd < k) return fail(h, AIDW_E_INSUFFICIENT_DATA, "nd = %lld < k = %d", (long long)h->nd, k);
+    CK(h, cudaSetDevice(h->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t ts = tsize(h->dt);
+    const size_t nb = ((size_t)nq * ts + 255) / 256 * 256;
+    s = ensure_work(h, 6 * nb + 256);
+    if (s != AIDW_OK) return s;
+    char *w = static_cast<char *>(h->work);
+    void *qx = w, *qy = w + nb, *robs = w + 2 * nb, *d1 = w + 3 * nb, *al = w + 4 * nb, *z = w + 5 * nb;
+    void *mm = w + 6 * nb;
+    CK(h, cudaMemcpyAsync(qx, qx_host, (size_t)nq * ts, cudaMemcpyHostToDevice, st));
+    CK(h, cudaMemcpyAsync(qy, qy_host, (size_t)nq * ts, cudaMemcpyHostToDevice, st));
+    if ((s = aidw_knn_robs(h, qx, qy, nq, k, robs, d1, mm, nullptr, stream)) != AIDW_OK) return s;
+    if ((s = aidw_alpha(h, robs, nq, alpha_lv, rb, r_min, r_max, mm, mf, al, stream)) != AIDW_OK) return s;
+    if ((s = aidw_interpolate(h, qx, qy, nq, al, d1, z, stream)) != AIDW_OK) return s;
+    CK(h, cudaMemcpyAsync(z_host, z, (size_t)nq * ts, cudaMemcpyDeviceToHost, st));
+    return aidw_check(h, stream);
+}
+
+aidw_status aidw_destroy(aidw_t h)
+{
+    if (!h) return AIDW_OK;
+    cudaSetDevice(h->device);
+    if (h->data || h->sc || h->work) cudaDeviceSynchronize();
+    if (h->data) cudaFree(h->data);
+    if (h->sc) cudaFree(h->sc);
+    if (h->work) cudaFree(h->work);
+    delete h;
+    return AIDW_OK;
+}
+
+}  // extern "C"

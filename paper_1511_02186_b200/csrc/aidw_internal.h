@@ -1,0 +1,49 @@
+// aidw_internal.h -- launchers shared by the C-ABI (aidw_api.cu) and the kernel
+// translation units.  Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace aidw {
+
+// Data tiles.  kTileW is also the fp32 accumulation block of the
+// weighting pass (fp32 sums within a tile, fp64 across tiles) -- part of the fp32
+// result's rounding, fixed so results do not depend on launch shape or GPU count.
+constexpr int kTileK = 1024;   // points per smem stage, kNN pass (x, y)
+constexpr int kStagesK = 4;
+constexpr int kTileW = 512;    // points per smem stage, weighting pass (x, y, z)
+constexpr int kStagesW = 4;
+constexpr int kPad = 1024;     // internal arrays padded to a multiple of both tiles
+
+// Device scratch owned by a handle.
+struct Scratch {
+    unsigned long long mn;      // ordered bits of min r_obs (identity ~0ull)
+    unsigned long long mx;      // ordered bits of max r_obs (identity 0)
+    unsigned int done;          // CTA ticket for the last-CTA finalise
+    unsigned int pad0;
+    long long err_idx;          // smallest non-finite query index (LLONG_MAX = none)
+    unsigned long long keys[4]; // bbox: ordered keys of min x, max x, min y, max y
+    unsigned long long nonfinite;
+};
+
+// Each launcher returns the number of kernels it launched (>= 0) or -1 on a
+// launch error (cudaGetLastError is left set for the caller).
+int launch_prep(int dtype, int layout, const void *src, int64_t nd, int64_t ndp, void *data,
+                Scratch *sc, cudaStream_t st);
+
+int launch_knn(int dtype, int k, const void *data, int64_t ndp, const void *qx, const void *qy,
+               int64_t nq, void *r_obs, void *d1sq, void *minmax, void *dists, Scratch *sc,
+               cudaStream_t st);
+
+int launch_minmax_identity(int dtype, void *minmax, cudaStream_t st);
+
+int launch_alpha(int dtype, const void *r_obs, int64_t nq, double r_exp, const double *lv,
+                 int rb, double rmin, double rmax, const void *minmax, int mf, void *alpha,
+                 cudaStream_t st);
+
+int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const void *qx,
+                  const void *qy, int64_t nq, const void *alpha, const void *d1sq, void *z,
+                  cudaStream_t st);
+
+}  // namespace aidw

@@ -1,0 +1,168 @@
+// alpha_prep.cu -- S0 (repack + bounding box) and S4 (R, mu_R, alpha) kernels.
+#include "aidw_internal.h"
+#include "device.cuh"
+
+namespace aidw {
+
+// ------------------------------------------------------------------ S0: prep
+// Order-preserving map double -> uint64 (for atomicMin/Max of signed values).
+__device__ __forceinline__ unsigned long long ord_key(double v)
+{
+    unsigned long long u = (unsigned long long)__double_as_longlong(v);
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t < v ? t : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
+}
+
+// Repack the user layout (SoA / AoS / AoaS) into the internal
+// padded SoA; padding points are (+inf, +inf, 0): never selected by the kNN,
+// weight 0 in Eq. 1.  Also the exact bbox min/max (for A, Eq. 2) and a
+// non-finite count.
+template <typename T>
+__global__ void prep_kernel(const T *__restrict__ src, int layout, int64_t nd, int64_t ndp,
+                            T *__restrict__ data, Scratch *sc)
+{
+    T *px = data, *py = data + ndp, *pz = data + 2 * ndp;
+    unsigned long long kx0 = ~0ull, kx1 = 0, ky0 = ~0ull, ky1 = 0, bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndp;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < nd) {
+            T x, y, z;
+            if (layout == 0) {
+                x = src[i];
+                y = src[nd + i];
+                z = src[2 * nd + i];
+            } else if (layout == 1) {
+                x = src[3 * i];
+                y = src[3 * i + 1];
+                z = src[3 * i + 2];
+            } else {
+                x = src[4 * i];
+                y = src[4 * i + 1];
+                z = src[4 * i + 2];
+            }
+            px[i] = x;
+            py[i] = y;
+            pz[i] = z;
+            if (!(isfinite(x) && isfinite(y) && isfinite(z))) ++bad;
+            const unsigned long long a = ord_key((double)x), b = ord_key((double)y);
+            kx0 = a < kx0 ? a : kx0;
+            kx1 = a > kx1 ? a : kx1;
+            ky0 = b < ky0 ? b : ky0;
+            ky1 = b > ky1 ? b : ky1;
+        } else {
+            px[i] = pos_inf<T>();
+            py[i] = pos_inf<T>();
+            pz[i] = T(0);
+        }
+    }
+    kx0 = warp_min_u64(kx0);
+    ky0 = warp_min_u64(ky0);
+    kx1 = warp_max_u64(kx1);
+    ky1 = warp_max_u64(ky1);
+    bad = __reduce_add_sync(0xffffffffu, (unsigned)bad);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&sc->keys[0], kx0);
+        atomicMax(&sc->keys[1], kx1);
+        atomicMin(&sc->keys[2], ky0);
+        atomicMax(&sc->keys[3], ky1);
+        if (bad) atomicAdd(&sc->nonfinite, bad);
+    }
+}
+
+int launch_prep(int dtype, int layout, const void *src, int64_t nd, int64_t ndp, void *data,
+                Scratch *sc, cudaStream_t st)
+{
+    const int threads = 256;
+    int64_t blocks = (ndp + threads - 1) / threads;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (dtype == 0)
+        prep_kernel<float><<<(unsigned)blocks, threads, 0, st>>>((const float *)src, layout, nd, ndp,
+                                                                  (float *)data, sc);
+    else
+        prep_kernel<double><<<(unsigned)blocks, threads, 0, st>>>((const double *)src, layout, nd, ndp,
+                                                                   (double *)data, sc);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// ------------------------------------------------------------------ S4: alpha
+struct Levels {
+    double a[5];
+};
+
+// Eq. 4, Eq. 5, Eq. 6,
+// all in fp64 (R24); intervals resolve first-match in printed order.
+template <typename T>
+__global__ void alpha_kernel(const T *__restrict__ robs, int64_t nq, double r_exp, Levels lv, int rb,
+                             double rmin, double rmax, const T *__restrict__ mm, int mf,
+                             T *__restrict__ alpha)
+{
+    if (rb == 0) {  // GLOBAL: bounds on r_obs -> bounds on R (division is monotone)
+        rmin = (double)(-mm[0]) / r_exp;
+        rmax = (double)mm[1] / r_exp;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double R = (double)robs[i] / r_exp;
+        double mu;
+        if (R <= rmin)
+            mu = 0.0;
+        else if (R <= rmax)
+            mu = (mf == 0) ? 0.5 - 0.5 * cospi((R - rmin) / (rmax - rmin))
+                           : 0.5 - 0.5 * cos(3.141592653589793 / rmax * (R - rmin));
+        else
+            mu = 1.0;
+        double al;
+        if (mu <= 0.1)
+            al = lv.a[0];
+        else if (mu <= 0.3)
+            al = lv.a[0] * (1.0 - 5.0 * (mu - 0.1)) + 5.0 * lv.a[1] * (mu - 0.1);
+        else if (mu <= 0.5)
+            al = 5.0 * lv.a[2] * (mu - 0.3) + lv.a[1] * (1.0 - 5.0 * (mu - 0.3));
+        else if (mu <= 0.7)
+            al = lv.a[2] * (1.0 - 5.0 * (mu - 0.5)) + 5.0 * lv.a[3] * (mu - 0.5);
+        else if (mu <= 0.9)
+            al = 5.0 * lv.a[4] * (mu - 0.7) + lv.a[3] * (1.0 - 5.0 * (mu - 0.7));
+        else
+            al = lv.a[4];
+        alpha[i] = (T)al;
+    }
+}
+
+int launch_alpha(int dtype, const void *r_obs, int64_t nq, double r_exp, const double *lvp, int rb,
+                 double rmin, double rmax, const void *minmax, int mf, void *alpha, cudaStream_t st)
+{
+    Levels lv;
+    for (int i = 0; i < 5; ++i) lv.a[i] = lvp[i];
+    const int threads = 256;
+    int64_t blocks = (nq + threads - 1) / threads;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (dtype == 0)
+        alpha_kernel<float><<<(unsigned)blocks, threads, 0, st>>>(
+            (const float *)r_obs, nq, r_exp, lv, rb, rmin, rmax, (const float *)minmax, mf, (float *)alpha);
+    else
+        alpha_kernel<double><<<(unsigned)blocks, threads, 0, st>>>(
+            (const double *)r_obs, nq, r_exp, lv, rb, rmin, rmax, (const double *)minmax, mf,
+            (double *)alpha);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+}  // namespace aidw

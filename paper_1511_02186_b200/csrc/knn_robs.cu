@@ -1,0 +1,289 @@
+// knn_robs.cu -- S1 + S2 of the AIDW hot path on sm_100a.
+//
+// Per query: the k smallest squared distances to ALL data points (brute force,
+// PAPER.md:317-340, §3.1.2 Steps 1-3 -- "if dist < the kth distance, then replace
+// the kth distance", strict <), then r_obs = (1/k) sum d_i (Eq. 3),
+// the nearest squared distance d1sq, and the {-min, max} of r_obs over the launch.
+//
+// B200 design -- the paper's "tiled" idea,
+// rebuilt for sm_100a:
+//  * data x/y tiles stream through a 4-stage shared-memory ring filled by the TMA
+//    engine (cp.async.bulk, one elected thread, mbarrier complete_tx), decoupled
+//    from the block size;
+//  * every thread owns Q queries; a data point is read from smem once (LDS.128
+//    broadcast, 4 points) and reused Q times from registers;
+//  * the top-k list lives in registers (compile-time K; k < K handled by -inf
+//    sentinels in the first K-k slots) and is updated by a branch-free min/max
+//    network, entered only behind warp-uniform votes -- after the first few
+//    thousand points insertions are rare, so the steady state is 4 FP32 ops +
+//    1 compare per pair;
+//  * the epilogue reduces min/max of r_obs with REDUX (fp32) / shuffles (fp64),
+//    one atomic per warp, and the last CTA writes {-min, max} ready for an
+//    allreduce(MAX) -- no extra launch.
+#include "aidw_internal.h"
+#include "device.cuh"
+
+#include <climits>
+
+namespace aidw {
+
+template <typename T> struct KnnArgs {
+    const T *px, *py;  // internal SoA, padded to ndp with +inf
+    int64_t ndp;
+    const T *qx, *qy;
+    int64_t nq;
+    int k;
+    T *r_obs, *d1sq, *minmax, *dists;
+    Scratch *sc;
+};
+
+__device__ __forceinline__ unsigned long long ord_bits(float v) { return (unsigned long long)__float_as_uint(v); }
+__device__ __forceinline__ unsigned long long ord_bits(double v) { return (unsigned long long)__double_as_longlong(v); }
+template <typename T> __device__ __forceinline__ T from_bits(unsigned long long b);
+template <> __device__ __forceinline__ float from_bits<float>(unsigned long long b) { return __uint_as_float((unsigned)b); }
+template <> __device__ __forceinline__ double from_bits<double>(unsigned long long b) { return __longlong_as_double((long long)b); }
+
+// Warp min/max of non-negative values via their (order-preserving) bit patterns.
+__device__ __forceinline__ void warp_minmax(float v, bool valid, unsigned long long &mn, unsigned long long &mx)
+{
+    unsigned b = __float_as_uint(v);
+    mn = __reduce_min_sync(0xffffffffu, valid ? b : 0xffffffffu);
+    mx = __reduce_max_sync(0xffffffffu, valid ? b : 0u);
+    if (mn == 0xffffffffu) mn = ~0ull;
+}
+
+__device__ __forceinline__ void warp_minmax(double v, bool valid, unsigned long long &mn, unsigned long long &mx)
+{
+    unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    mn = valid ? b : ~0ull;
+    mx = valid ? b : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long a = __shfl_xor_sync(0xffffffffu, mn, o);
+        unsigned long long c = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn;
+        mx = c > mx ? c : mx;
+    }
+}
+
+// Sorted insertion of s into ascending b[0..K-1], dropping the largest:
+// b'[i] = min(b[i], max(b[i-1], s)), b'[0] = min(b[0], s).  Equivalent to Step 3's
+// replace-the-kth-then-bubble for s < b[K-1]; a no-op otherwise.
+template <typename T, int K>
+__device__ __forceinline__ void topk_insert(T (&b)[K], T s)
+{
+#pragma unroll
+    for (int i = K - 1; i > 0; --i) b[i] = tmin(b[i], tmax(b[i - 1], s));
+    b[0] = tmin(b[0], s);
+}
+
+template <typename T, int K, int Q>
+__global__ void __launch_bounds__(kBlock) knn_robs_kernel(const KnnArgs<T> a)
+{
+    constexpr int TILE = kTileK, STAGES = kStagesK;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T *sx = reinterpret_cast<T *>(smem_raw);
+    T *sy = sx + STAGES * TILE;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sy + STAGES * TILE);
+    uint64_t *empty = full + STAGES;
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int ntiles = (int)(a.ndp / TILE);
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    auto issue = [&](int tile, int slot) {
+        mbar_arrive_expect_tx(&full[slot], 2u * TILE * sizeof(T));
+        bulk_g2s(sx + slot * TILE, a.px + (int64_t)tile * TILE, TILE * sizeof(T), &full[slot]);
+        bulk_g2s(sy + slot * TILE, a.py + (int64_t)tile * TILE, TILE * sizeof(T), &full[slot]);
+    };
+    if (tid == 0)
+        for (int s = 0; s < STAGES && s < ntiles; ++s) issue(s, s);
+
+    // ---- queries owned by this thread (strided by the block for coalescing)
+    const int64_t base = (int64_t)blockIdx.x * (kBlock * Q) + tid;
+    T qx[Q], qy[Q];
+    bool valid[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int64_t idx = base + q * kBlock;
+        valid[q] = idx < a.nq;
+        qx[q] = valid[q] ? a.qx[idx] : T(0);
+        qy[q] = valid[q] ? a.qy[idx] : T(0);
+        if (valid[q] && !(isfinite(qx[q]) && isfinite(qy[q])))
+            atomicMin(&a.sc->err_idx, (long long)idx);
+    }
+
+    // ---- register top-K; slots [0, K-k) hold -inf sentinels (never displaced)
+    T buf[Q][K];
+    const int k0 = K - a.k;
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int i = 0; i < K; ++i) buf[q][i] = (i < k0) ? -pos_inf<T>() : pos_inf<T>();
+
+    for (int t = 0; t < ntiles; ++t) {
+        const int slot = t % STAGES;
+        const uint32_t par = (uint32_t)(t / STAGES) & 1u;
+        mbar_wait(&full[slot], par);
+        const T *tx = sx + slot * TILE;
+        const T *ty = sy + slot * TILE;
+#pragma unroll 2
+        for (int j = 0; j < TILE; j += 4) {
+            const Vec4<T> X = lds4(tx + j), Y = lds4(ty + j);
+            T s[Q][4];
+            bool hit = false;
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    s[q][e] = dist_sq(qx[q], qy[q], X.v[e], Y.v[e]);
+                    hit |= s[q][e] < buf[q][K - 1];
+                }
+            if (__any_sync(0xffffffffu, hit)) {
+                // points in index order; each query's list updated in order
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
+                        const bool h = s[q][e] < buf[q][K - 1];
+                        if (__any_sync(0xffffffffu, h)) {
+                            if (h) topk_insert<T, K>(buf[q], s[q][e]);
+                        }
+                    }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (tid == 0 && t + STAGES < ntiles) {
+            mbar_wait(&empty[slot], par);
+            issue(t + STAGES, slot);
+        }
+    }
+
+    // ---- epilogue: r_obs (Eq. 3), d1sq, k distances, min/max
+    T robs_l[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        T sum = T(0), d1 = buf[q][K - 1];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            if (i >= k0) sum = add_rn(sum, sqrt_rn(buf[q][i]));  // ascending order
+            if (i == k0) d1 = buf[q][i];
+        }
+        const T robs = div_rn(sum, (T)a.k);
+        robs_l[q] = robs;
+        const int64_t idx = base + q * kBlock;
+        if (valid[q]) {
+            a.r_obs[idx] = robs;
+            if (a.d1sq) a.d1sq[idx] = d1;
+            if (a.dists) {
+                T *o = a.dists + idx * a.k;
+#pragma unroll
+                for (int i = 0; i < K; ++i)
+                    if (i >= k0) o[i - k0] = sqrt_rn(buf[q][i]);
+            }
+        }
+    }
+
+    if (a.minmax) {
+        unsigned long long mn = ~0ull, mx = 0ull;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            unsigned long long m0, m1;
+            warp_minmax(robs_l[q], valid[q], m0, m1);
+            mn = m0 < mn ? m0 : mn;
+            mx = m1 > mx ? m1 : mx;
+        }
+        if (lane == 0) {
+            if (mn != ~0ull) atomicMin(&a.sc->mn, mn);
+            atomicMax(&a.sc->mx, mx);
+            __threadfence();
+        }
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            const unsigned ticket = atomicAdd(&a.sc->done, 1u);
+            if (ticket == gridDim.x - 1) {  // last CTA: publish and reset the scratch
+                __threadfence();
+                const unsigned long long gmn = atomicAdd(&a.sc->mn, 0ull);
+                const unsigned long long gmx = atomicAdd(&a.sc->mx, 0ull);
+                a.minmax[0] = -from_bits<T>(gmn);
+                a.minmax[1] = from_bits<T>(gmx);
+                a.sc->mn = ~0ull;
+                a.sc->mx = 0ull;
+                a.sc->done = 0u;
+                __threadfence();
+            }
+        }
+    }
+}
+
+template <typename T> __global__ void minmax_identity_kernel(T *mm)
+{
+    mm[0] = -pos_inf<T>();
+    mm[1] = -pos_inf<T>();
+}
+
+template <typename T, int K, int Q>
+static int launch_knn_t(const KnnArgs<T> &a, cudaStream_t st)
+{
+    const size_t smem = (size_t)2 * kStagesK * kTileK * sizeof(T) + 2 * kStagesK * sizeof(uint64_t);
+    if (cudaFuncSetAttribute(knn_robs_kernel<T, K, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return -1;
+    const int64_t per_cta = (int64_t)kBlock * Q;
+    const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
+    knn_robs_kernel<T, K, Q><<<grid, kBlock, smem, st>>>(a);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+template <typename T>
+static int dispatch_k(const KnnArgs<T> &a, cudaStream_t st)
+{
+    const int k = a.k;
+    if (k <= 1) return launch_knn_t<T, 1, 2>(a, st);
+    if (k <= 2) return launch_knn_t<T, 2, 2>(a, st);
+    if (k <= 4) return launch_knn_t<T, 4, 2>(a, st);
+    if (k <= 8) return launch_knn_t<T, 8, 2>(a, st);
+    if (k <= 10) return launch_knn_t<T, 10, 2>(a, st);
+    if (k <= 12) return launch_knn_t<T, 12, 2>(a, st);
+    if (k <= 15) return launch_knn_t<T, 15, 2>(a, st);
+    if (k <= 16) return launch_knn_t<T, 16, 2>(a, st);
+    if (k <= 24) return launch_knn_t<T, 24, 1>(a, st);
+    return launch_knn_t<T, 32, 1>(a, st);
+}
+
+int launch_knn(int dtype, int k, const void *data, int64_t ndp, const void *qx, const void *qy,
+               int64_t nq, void *r_obs, void *d1sq, void *minmax, void *dists, Scratch *sc,
+               cudaStream_t st)
+{
+    if (dtype == 0) {
+        const float *p = static_cast<const float *>(data);
+        KnnArgs<float> a{p, p + ndp, ndp, (const float *)qx, (const float *)qy, nq, k,
+                         (float *)r_obs, (float *)d1sq, (float *)minmax, (float *)dists, sc};
+        return dispatch_k(a, st);
+    }
+    const double *p = static_cast<const double *>(data);
+    KnnArgs<double> a{p, p + ndp, ndp, (const double *)qx, (const double *)qy, nq, k,
+                      (double *)r_obs, (double *)d1sq, (double *)minmax, (double *)dists, sc};
+    return dispatch_k(a, st);
+}
+
+int launch_minmax_identity(int dtype, void *minmax, cudaStream_t st)
+{
+    if (dtype == 0)
+        minmax_identity_kernel<float><<<1, 1, 0, st>>>((float *)minmax);
+    else
+        minmax_identity_kernel<double><<<1, 1, 0, st>>>((double *)minmax);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+}  // namespace aidw

@@ -1,0 +1,295 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by
+element on the same seeded inputs.
+
+Bars (north star): kNN distance multisets and r_obs bit-exact at the kernel's
+precision (fp32 vs the oracle's float instantiation, fp64 vs fp64); Z within
+relative 1e-4 (fp32) / 1e-10 (fp64) of the fp64 oracle.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import datagen
+
+pytestmark = pytest.mark.gpu
+
+LV = datagen.ALPHA_LEVELS
+TOL = {torch.float32: 1e-4, torch.float64: 1e-10}
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1511_02186_b200 as P
+    P.build_extension()
+    P.lib()
+    return P
+
+
+def rel_err(got, want):
+    got = np.asarray(got, np.float64)
+    return np.abs(got - want) / np.abs(want)
+
+
+def gpu_knn(P, eng, qx, qy, k):
+    r, d1, mm, d = eng.knn_robs(torch.as_tensor(qx), torch.as_tensor(qy), k, want_dists=True)
+    torch.cuda.synchronize()
+    eng.check()
+    return r.cpu().numpy(), d1.cpu().numpy(), mm.cpu().numpy(), d.cpu().numpy()
+
+
+def oracle_knn(orc, x, y, qx, qy, k, dtype):
+    if dtype == torch.float32:
+        return orc.knn_f32(x, y, qx, qy, k, want_dists=True)
+    return orc.knn_f64(x, y, qx, qy, k, want_dists=True)
+
+
+def check_full(P, orc, x, y, z, qx, qy, k, dtype, modes=("global", "fixed")):
+    eng = P.AIDW(x, y, z, dtype=dtype)
+    # r_exp: same Eq. 2 in fp64 on both sides
+    assert eng.r_exp == orc.r_exp(len(x), orc.bbox_area(x, y))
+    r, d1, mm, d = gpu_knn(P, eng, qx, qy, k)
+    ro, do = oracle_knn(orc, x, y, qx, qy, k, dtype)
+    assert np.array_equal(d, do), "kNN distance multisets differ"
+    assert np.array_equal(r, ro), "r_obs differs"
+    assert np.array_equal(np.sqrt(d1), do[:, 0])  # d1sq is the nearest s
+    assert mm[0] == -r.min() and mm[1] == r.max()
+    for mode in modes:
+        rb = P.GLOBAL if mode == "global" else P.FIXED
+        Zg = eng.run(qx, qy, k, LV, rb).cpu().numpy()
+        eng.check()
+        Zo = orc.aidw(x, y, z, qx, qy, k, LV, mode=mode)
+        e = rel_err(Zg, Zo)
+        assert e.max() <= TOL[dtype], (mode, e.max(), int(e.argmax()))
+    eng.close()
+    return e
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_C1(P, orc, dtype):
+    x, y, z = datagen.make_data("C1")
+    qx, qy = datagen.make_queries("C1")
+    check_full(P, orc, x, y, z, qx, qy, 10, dtype)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_C2(P, orc, dtype):
+    x, y, z = datagen.make_data("C2")
+    qx, qy = datagen.make_queries("C2")
+    check_full(P, orc, x, y, z, qx, qy, 10, dtype)
+
+
+def test_C3_clustered(P, orc):
+    """100K x 100K, k = 15, clustered: kNN bit-exact on every query; Z (GLOBAL bounds
+    from the full oracle kNN) on a strided subset."""
+    x, y, z = datagen.make_data("C3")
+    qx, qy = datagen.make_queries("C3")
+    eng = P.AIDW(x, y, z, dtype=torch.float32)
+    r, d1, mm, d = gpu_knn(P, eng, qx, qy, 15)
+    ro, do = orc.knn_f32(x, y, qx, qy, 15, want_dists=True)
+    assert np.array_equal(d, do) and np.array_equal(r, ro)
+    z_g = eng.run(qx, qy, 15, LV, P.GLOBAL).cpu().numpy()
+    # oracle: fp64 r_obs for all queries (GLOBAL bounds), Z on every 97th query
+    re = orc.r_exp(len(x), orc.bbox_area(x, y))
+    robs64 = orc.knn_f64(x, y, qx, qy, 15)
+    rmin, rmax = orc.r_bounds(robs64, re, orc.GLOBAL)
+    sub = np.arange(0, len(qx), 97)
+    a = orc.alpha(robs64[sub], re, LV, rmin, rmax)
+    Zo = orc.idw(x, y, z, qx[sub], qy[sub], a)
+    e = rel_err(z_g[sub], Zo)
+    assert e.max() <= 1e-4, e.max()
+
+
+def test_C4_full_size_sampled(P, orc):
+    """1M x 1M fp32 in the bench's launch configuration: kNN + r_obs bit-exact and Z
+    (FIXED bounds: per-query, so the oracle computes sampled queries one by one) on a
+    strided sample; GLOBAL: {-min, max} equals the min/max of the full r_obs array and
+    sampled alpha / Z follow from it."""
+    x, y, z = datagen.make_data("C4")
+    qx, qy = datagen.make_queries("C4")
+    eng = P.AIDW(x, y, z, dtype=torch.float32)
+    Q = lambda v: torch.as_tensor(v, dtype=torch.float32, device="cuda")
+    tqx, tqy = Q(qx), Q(qy)
+    r, d1, mm = eng.knn_robs(tqx, tqy, 10)
+    sub = np.concatenate([np.arange(0, len(qx), 16001), [len(qx) - 1]])
+    ro, do = orc.knn_f32(x, y, qx[sub], qy[sub], 10, want_dists=True)
+    assert np.array_equal(r.cpu().numpy()[sub], ro)
+    assert np.array_equal(np.sqrt(d1.cpu().numpy()[sub]), do[:, 0])
+    rc = r.cpu().numpy()
+    mmc = mm.cpu().numpy()
+    assert mmc[0] == -rc.min() and mmc[1] == rc.max()
+    # FIXED (0, 2): full oracle chain on the sample
+    a_f = eng.alpha(r, LV, P.FIXED, 0.0, 2.0, mm)
+    z_f = eng.interpolate(tqx, tqy, a_f, d1).cpu().numpy()
+    Zo = orc.aidw(x, y, z, qx[sub], qy[sub], 10, LV, mode="fixed")
+    assert rel_err(z_f[sub], Zo).max() <= 1e-4
+    # GLOBAL: bounds verified above as the exact min/max of r_obs; sampled alpha, Z
+    a_g = eng.alpha(r, LV, P.GLOBAL, 0, 0, mm)
+    z_g = eng.interpolate(tqx, tqy, a_g, d1).cpu().numpy()
+    re = eng.r_exp
+    ro64 = orc.knn_f64(x, y, qx[sub], qy[sub], 10)
+    a_o = orc.alpha(ro64, re, LV, -float(mmc[0]) / re, float(mmc[1]) / re)
+    assert np.max(np.abs(a_g.cpu().numpy()[sub] - a_o)) < 1e-5
+    Zo = orc.idw(x, y, z, qx[sub], qy[sub], a_o)
+    assert rel_err(z_g[sub], Zo).max() <= 1e-4
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("nd,nq,k", [(5, 7, 5), (1, 3, 1), (1500, 1, 3), (3001, 777, 32), (2049, 300, 1),
+                                     (4096, 513, 16)])
+def test_ragged_and_k_range(P, orc, dtype, nd, nq, k):
+    x, y, z, qx, qy = datagen.random_cloud(nd * 7 + nq, nd, nq)
+    if nd == 1:
+        eng = P.AIDW(x, y, z, dtype=dtype, area=1.0)
+        r, d1, mm, d = gpu_knn(P, eng, qx, qy, k)
+        ro, do = oracle_knn(orc, x, y, qx, qy, k, dtype)
+        assert np.array_equal(d, do)
+        Zg = eng.run(qx, qy, k, LV, P.GLOBAL).cpu().numpy()
+        assert rel_err(Zg, np.full(nq, z[0])).max() <= TOL[dtype]
+        return
+    check_full(P, orc, x, y, z, qx, qy, k, dtype)
+
+
+def test_empty_queries(P):
+    x, y, z, _, _ = datagen.random_cloud(3, 100, 1)
+    eng = P.AIDW(x, y, z)
+    e = torch.empty(0, device="cuda")
+    r, d1, mm = eng.knn_robs(e, e, 10)
+    assert r.numel() == 0 and mm.cpu().tolist() == [-math.inf, -math.inf]
+    assert eng.run(e, e, 10).numel() == 0
+
+
+def test_single_query_global_is_alpha1(P, orc):
+    """nq = 1 in GLOBAL mode: R_max == R_min, row 1 of Eq. 5 -> mu = 0 -> alpha_1 (R10)."""
+    x, y, z, qx, qy = datagen.random_cloud(8, 2000, 1)
+    eng = P.AIDW(x, y, z, dtype=torch.float64)
+    _, t = eng.run(qx, qy, 10, LV, P.GLOBAL, trace=True)
+    assert t["alpha"].item() == LV[0]
+    Zo = orc.aidw(x, y, z, qx, qy, 10, LV, mode="global")
+    assert rel_err(eng.run(qx, qy, 10).cpu().numpy(), Zo).max() < 1e-10
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_coincident_queries(P, orc, dtype):
+    """Queries at data points reproduce z exactly; duplicated data points give their mean."""
+    x, y, z, qx, qy = datagen.random_cloud(31, 3000, 64)
+    x = np.concatenate([x, x[:5]])
+    y = np.concatenate([y, y[:5]])
+    z = np.concatenate([z, z[5:10]])  # duplicates of points 0..4 with other values
+    qx = np.concatenate([qx, x[:20]])
+    qy = np.concatenate([qy, y[:20]])
+    eng = P.AIDW(x, y, z, dtype=dtype)
+    Zg = eng.run(qx, qy, 10, LV).cpu().numpy().astype(np.float64)
+    Zo = orc.aidw(x, y, z, qx, qy, 10, LV)
+    assert rel_err(Zg, Zo).max() <= TOL[dtype]
+    zt = z.astype(np.float32) if dtype == torch.float32 else z
+    assert np.array_equal(Zg[64 + 5:], zt[5:20].astype(np.float64))
+    assert np.allclose(Zg[64:69], (z[:5] + z[5:10]) / 2, rtol=TOL[dtype])
+
+
+def test_layouts_identical(P):
+    x, y, z, qx, qy = datagen.random_cloud(2, 5000, 300)
+    outs = []
+    for lay in (P.SOA, P.AOS, P.AOAS):
+        if lay == P.SOA:
+            buf = np.concatenate([x, y, z])
+        elif lay == P.AOS:
+            buf = np.stack([x, y, z], 1).reshape(-1)
+        else:
+            buf = np.stack([x, y, z, np.zeros_like(x)], 1).reshape(-1)
+        t = torch.as_tensor(buf, dtype=torch.float32, device="cuda")
+        h = P.aidw_create(t, len(x), P.F32, lay)
+        q = lambda v: torch.as_tensor(v, dtype=torch.float32, device="cuda")
+        r, d1, mm = torch.empty(300, device="cuda"), torch.empty(300, device="cuda"), torch.empty(2, device="cuda")
+        P.aidw_knn_robs(h, q(qx), q(qy), 10, r, d1, mm)
+        a = torch.empty(300, device="cuda")
+        P.aidw_alpha(h, r, LV, P.GLOBAL, 0, 0, mm, P.NORMALIZED, a)
+        zz = torch.empty(300, device="cuda")
+        P.aidw_interpolate(h, q(qx), q(qy), a, d1, zz)
+        torch.cuda.synchronize()
+        P.aidw_destroy(h)
+        outs.append(zz.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+def test_constant_levels_is_idw_and_convex(P, orc):
+    x, y, z, qx, qy = datagen.random_cloud(17, 20000, 2000)
+    eng = P.AIDW(x, y, z)
+    Zg = eng.run(qx, qy, 10, [2.0] * 5).cpu().numpy()
+    Zi = orc.idw(x, y, z, qx, qy, 2.0)
+    assert rel_err(Zg, Zi).max() <= 1e-4
+    assert Zg.min() >= np.float32(z.min()) and Zg.max() <= np.float32(z.max())
+    # d1sq omitted -> computed internally; same result
+    a = torch.full((2000,), 2.0, device="cuda")
+    Zn = eng.interpolate(qx, qy, a, None).cpu().numpy()
+    assert np.array_equal(Zn, Zg)
+
+
+def test_sharding_bit_identical(P):
+    """Per-query results do not depend on how queries are sharded (1/2/4/8 'GPUs'
+    emulated on one device, GLOBAL bounds combined by MAX as the allreduce does)."""
+    x, y, z, qx, qy = datagen.random_cloud(23, 30000, 4099)
+    eng = P.AIDW(x, y, z)
+    ref = eng.run(qx, qy, 10, LV, P.GLOBAL).cpu().numpy()
+    from paper_1511_02186_b200.partition import shard
+    for world in (2, 4, 8):
+        parts = []
+        mms = []
+        for rnk in range(world):
+            s, e = shard(len(qx), rnk, world)
+            parts.append(eng.knn_robs(qx[s:e], qy[s:e], 10))
+            mms.append(parts[-1][2])
+        mm = torch.stack(mms).max(0).values
+        zs = []
+        for rnk in range(world):
+            s, e = shard(len(qx), rnk, world)
+            r, d1, _ = parts[rnk]
+            a = eng.alpha(r, LV, P.GLOBAL, 0, 0, mm)
+            zs.append(eng.interpolate(qx[s:e], qy[s:e], a, d1).cpu().numpy())
+        assert np.array_equal(np.concatenate(zs), ref), world
+
+
+def test_errors(P):
+    x, y, z, qx, qy = datagen.random_cloud(1, 100, 10)
+    with pytest.raises(P.AidwError, match="DEGENERATE"):
+        P.AIDW(x, np.zeros_like(x), z)
+    with pytest.raises(P.AidwError, match="NONFINITE"):
+        P.AIDW(np.where(np.arange(100) == 5, np.nan, x), y, z)
+    with pytest.raises(P.AidwError, match="INSUFFICIENT"):
+        P.AIDW(x[:5], y[:5], z[:5]).knn_robs(qx, qy, 10)
+    eng = P.AIDW(x, y, z)
+    with pytest.raises(P.AidwError, match="UNSUPPORTED"):
+        eng.knn_robs(qx, qy, 33)
+    r, d1, mm = eng.knn_robs(qx, qy, 10)
+    with pytest.raises(P.AidwError, match="BOUNDS"):
+        eng.alpha(r, LV, P.FIXED, 2.0, 2.0, mm)
+    with pytest.raises(P.AidwError, match="INVALID_ARG"):
+        eng.alpha(r, [1, 2, 3, 4, -1], P.GLOBAL, 0, 0, mm)
+    bad = qx.copy()
+    bad[7] = np.inf
+    bad[3] = np.nan
+    eng.knn_robs(bad, qy, 10)
+    with pytest.raises(P.AidwError, match="index 3"):
+        eng.check()
+    eng.check()  # cleared
+
+
+def test_run_host_matches_device(P):
+    x, y, z, qx, qy = datagen.random_cloud(41, 8000, 1000)
+    eng = P.AIDW(x, y, z)
+    zd = eng.run(qx, qy, 10, LV).cpu()
+    zh = eng.run_host(torch.as_tensor(qx, dtype=torch.float32).pin_memory(),
+                      torch.as_tensor(qy, dtype=torch.float32).pin_memory(), 10, LV)
+    assert torch.equal(zd, zh)
+
+
+def test_launch_count(P):
+    x, y, z, qx, qy = datagen.random_cloud(43, 3000, 500)
+    eng = P.AIDW(x, y, z)
+    n0 = eng.launches
+    eng.run(qx, qy, 10)
+    assert eng.launches - n0 == 3  # knn_robs, alpha, interpolate

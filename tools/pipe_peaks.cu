@@ -1,0 +1,67 @@
+// pipe_peaks.cu -- microbenchmark of the per-SM pipe rates the AIDW roofline uses
+// (SURVEY.md H6): MUFU ex2 / lg2 and FP32 FFMA throughput per SM
+// per clock on this B200.  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3
+// tools/pipe_peaks.cu -o pipe_peaks ; prints one JSON line.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int kIters = 4096;
+constexpr int kChains = 8;
+
+__device__ __forceinline__ float ex2(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float lg2(float x) { float y; asm volatile("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+
+struct Clk { unsigned long long c0, c1, t0, t1; };
+
+__device__ __forceinline__ unsigned long long gtime() { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
+
+template <int MODE>
+__global__ void bench(float *out, Clk *clk, float seed)
+{
+    float v[kChains];
+#pragma unroll
+    for (int i = 0; i < kChains; ++i) v[i] = seed + threadIdx.x * 1e-7f + i * 1e-3f;
+    unsigned long long c0 = clock64(), t0 = gtime();
+    for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+        for (int i = 0; i < kChains; ++i) {
+            if (MODE == 0) v[i] = ex2(v[i]);                 // MUFU.EX2
+            else if (MODE == 1) v[i] = lg2(v[i]);            // MUFU.LG2
+            else v[i] = fmaf(v[i], 1.0000001f, 1e-7f);       // FFMA
+        }
+    }
+    unsigned long long c1 = clock64(), t1 = gtime();
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < kChains; ++i) s += v[i];
+    if (s == 12345.f) out[0] = s;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *clk = Clk{c0, c1, t0, t1};
+}
+
+template <int MODE> static double run(int sms, float *out, Clk *clk, double *mhz)
+{
+    const int threads = 1024, blocks = sms * 2;
+    bench<MODE><<<blocks, threads>>>(out, clk, 0.5f);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaEventRecord(a);
+    bench<MODE><<<blocks, threads>>>(out, clk, 0.5f);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    Clk h; cudaMemcpy(&h, clk, sizeof h, cudaMemcpyDeviceToHost);
+    *mhz = (double)(h.c1 - h.c0) / (double)(h.t1 - h.t0) * 1e3;  // cycles per ns -> MHz
+    const double ops = (double)blocks * threads * kIters * kChains;
+    return ops / (ms * 1e-3) / (*mhz * 1e6) / sms;  // ops per clock per SM
+}
+
+int main()
+{
+    int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    float *out; Clk *clk; cudaMalloc(&out, 4); cudaMalloc(&clk, sizeof(Clk));
+    double m0, m1, m2;
+    double ex = run<0>(sms, out, clk, &m0), lg = run<1>(sms, out, clk, &m1), fm = run<2>(sms, out, clk, &m2);
+    printf("{\"sms\": %d, \"mufu_ex2_per_clk_sm\": %.2f, \"mufu_lg2_per_clk_sm\": %.2f, \"ffma_per_clk_sm\": %.2f, "
+           "\"sm_mhz_during\": [%.0f, %.0f, %.0f]}\n", sms, ex, lg, fm, m0, m1, m2);
+    return 0;
+}
