@@ -53,7 +53,10 @@ def run_sharded(engine, qx, qy, k, levels, rbounds=GLOBAL, r_min=0.0, r_max=2.0,
 def gather(z_local: torch.Tensor, nq: int, group=None) -> torch.Tensor:
     """Optional all-gather of the per-rank Z blocks into the full [nq] result."""
     world = dist.get_world_size(group)
-    sizes = [shard(nq, r, world) for r in range(world)]
-    parts = [torch.empty(e - s, dtype=z_local.dtype, device=z_local.device) for s, e in sizes]
-    dist.all_gather(parts, z_local.contiguous(), group=group)
-    return torch.cat(parts)
+    sizes = [e - s for s, e in (shard(nq, r, world) for r in range(world))]
+    m = max(sizes)
+    buf = torch.zeros(m, dtype=z_local.dtype, device=z_local.device)  # equal-size blocks
+    buf[: z_local.numel()] = z_local
+    parts = [torch.empty(m, dtype=z_local.dtype, device=z_local.device) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    return torch.cat([p[:n] for p, n in zip(parts, sizes)])
