@@ -14,6 +14,9 @@
 // Q queries per thread, every data point read once from smem per Q pairs.
 #include "aidw_internal.h"
 #include "device.cuh"
+#include "packed.cuh"
+
+#include <cstdlib>
 
 namespace aidw {
 
@@ -153,6 +156,186 @@ static int launch_interp_t(const InterpArgs<T> &a, cudaStream_t st)
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
+
+// ---------------------------------------------------------------------------------
+// fp32 weighting pass with packed fp32x2 arithmetic (FADD2/FMUL2/FFMA2).  Two
+// consecutive data points of one query form a "couple" evaluated in one packed
+// register pair; the fp32 tile sums are kept as {even, odd} partial sums and folded
+// into fp64 at every tile flush (R21).  The ex2 of couple (q, h) runs on
+// the FMA pipe (exp2_poly2) when bit (2q + h) of EMU is set, on the SFU otherwise:
+// this balances the SFU (8 issue-cycles per warp op) against the issue slot
+// (DESIGN.md §4.3).
+template <int Q, unsigned EMU>
+__global__ void __launch_bounds__(kBlock) interp_f32x2_kernel(const InterpArgs<float> a)
+{
+    constexpr int TILE = kTileW, STAGES = kStagesW;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *sx = reinterpret_cast<float *>(smem_raw);
+    float *sy = sx + STAGES * TILE;
+    float *sz = sy + STAGES * TILE;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sz + STAGES * TILE);
+    uint64_t *empty = full + STAGES;
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int ntiles = (int)(a.ndp / TILE);
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    auto issue = [&](int tile, int slot) {
+        mbar_arrive_expect_tx(&full[slot], 3u * TILE * sizeof(float));
+        const int64_t off = (int64_t)tile * TILE;
+        bulk_g2s(sx + slot * TILE, a.px + off, TILE * sizeof(float), &full[slot]);
+        bulk_g2s(sy + slot * TILE, a.py + off, TILE * sizeof(float), &full[slot]);
+        bulk_g2s(sz + slot * TILE, a.pz + off, TILE * sizeof(float), &full[slot]);
+    };
+    if (tid == 0)
+        for (int s = 0; s < STAGES && s < ntiles; ++s) issue(s, s);
+
+    const int64_t base = (int64_t)blockIdx.x * (kBlock * Q) + tid;
+    float qx[Q], qy[Q], d1[Q];
+    f32x2 QX[Q], QY[Q], C[Q], B[Q];
+    bool valid[Q];
+    double SW[Q], SWZ[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int64_t idx = base + q * kBlock;
+        valid[q] = idx < a.nq;
+        qx[q] = valid[q] ? a.qx[idx] : 0.f;
+        qy[q] = valid[q] ? a.qy[idx] : 0.f;
+        const float al = valid[q] ? a.alpha[idx] : 1.f;
+        d1[q] = valid[q] ? a.d1sq[idx] : 1.f;
+        const float c = -0.5f * al;
+        const float b = 0.5f * al * lg2_approx_noftz(d1[q]);
+        QX[q] = splat2(qx[q]);
+        QY[q] = splat2(qy[q]);
+        C[q] = splat2(c);
+        B[q] = splat2(b);
+        SW[q] = 0.0;
+        SWZ[q] = 0.0;
+    }
+
+    for (int t = 0; t < ntiles; ++t) {
+        const int slot = t % STAGES;
+        const uint32_t par = (uint32_t)(t / STAGES) & 1u;
+        mbar_wait(&full[slot], par);
+        const float *tx = sx + slot * TILE;
+        const float *ty = sy + slot * TILE;
+        const float *tz = sz + slot * TILE;
+        f32x2 sw[Q], swz[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) sw[q] = swz[q] = 0ull;
+#pragma unroll 2
+        for (int j = 0; j < TILE; j += 4) {
+            const float4 X = *reinterpret_cast<const float4 *>(tx + j);
+            const float4 Y = *reinterpret_cast<const float4 *>(ty + j);
+            const float4 Z = *reinterpret_cast<const float4 *>(tz + j);
+            const f32x2 Xh[2] = {pack2(X.x, X.y), pack2(X.z, X.w)};
+            const f32x2 Yh[2] = {pack2(Y.x, Y.y), pack2(Y.z, Y.w)};
+            const f32x2 Zh[2] = {pack2(Z.x, Z.y), pack2(Z.z, Z.w)};
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    const f32x2 dx = sub2(QX[q], Xh[h]);
+                    const f32x2 dy = sub2(QY[q], Yh[h]);
+                    const f32x2 s = fma2(dx, dx, mul2(dy, dy));
+                    float s0, s1;
+                    unpack2(s, s0, s1);
+                    const f32x2 l = pack2(lg2_approx(s0), lg2_approx(s1));
+                    const f32x2 e = fma2(C[q], l, B[q]);
+                    f32x2 w;
+                    if (EMU & (1u << (2 * q + h))) {
+                        w = exp2_poly2(e);
+                    } else {
+                        float e0, e1;
+                        unpack2(e, e0, e1);
+                        w = pack2(ex2_approx(e0), ex2_approx(e1));
+                    }
+                    sw[q] = add2(sw[q], w);
+                    swz[q] = fma2(w, Zh[h], swz[q]);
+                }
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            float w0, w1, z0, z1;
+            unpack2(sw[q], w0, w1);
+            unpack2(swz[q], z0, z1);
+            SW[q] += (double)w0 + (double)w1;
+            SWZ[q] += (double)z0 + (double)z1;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (tid == 0 && t + STAGES < ntiles) {
+            mbar_wait(&empty[slot], par);
+            issue(t + STAGES, slot);
+        }
+    }
+
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        if (!valid[q]) continue;
+        const int64_t idx = base + q * kBlock;
+        double zq = SWZ[q] / SW[q];
+        if (d1[q] == 0.f) {  // exact coincidence (R19)
+            double zc = 0.0;
+            long long cnt = 0;
+            for (int64_t i = 0; i < a.nd; ++i)
+                if (dist_sq(qx[q], qy[q], a.px[i], a.py[i]) == 0.f) {
+                    zc += (double)a.pz[i];
+                    ++cnt;
+                }
+            zq = zc / (double)cnt;
+        }
+        a.z[idx] = (float)zq;
+    }
+}
+
+template <int Q, unsigned EMU>
+static int launch_interp_f32x2(const InterpArgs<float> &a, cudaStream_t st)
+{
+    const size_t smem = (size_t)3 * kStagesW * kTileW * sizeof(float) + 2 * kStagesW * sizeof(uint64_t);
+    if (cudaFuncSetAttribute(interp_f32x2_kernel<Q, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return -1;
+    const int64_t per_cta = (int64_t)kBlock * Q;
+    const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
+    interp_f32x2_kernel<Q, EMU><<<grid, kBlock, smem, st>>>(a);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// Variant selection for tuning (AIDW_INTERP_VARIANT); 0 = default.
+static int interp_variant()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("AIDW_INTERP_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
+static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st)
+{
+    switch (interp_variant()) {
+    case 1: return launch_interp_t<float, 2>(a, st);         // scalar, all-SFU
+    case 2: return launch_interp_f32x2<2, 0x0>(a, st);       // packed, all-SFU
+    case 3: return launch_interp_f32x2<2, 0x5>(a, st);       // packed, 2 of 4 couples emulated
+    case 4: return launch_interp_f32x2<2, 0x7>(a, st);       // 3 of 4
+    case 5: return launch_interp_f32x2<2, 0xF>(a, st);       // 4 of 4
+    case 6: return launch_interp_f32x2<4, 0x77>(a, st);      // Q=4, 6 of 8
+    case 7: return launch_interp_f32x2<4, 0x7F>(a, st);      // Q=4, 7 of 8
+    case 8: return launch_interp_f32x2<4, 0x55>(a, st);      // Q=4, 4 of 8
+    default: return launch_interp_f32x2<2, 0x7>(a, st);
+    }
+}
+
 int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const void *qx,
                   const void *qy, int64_t nq, const void *alpha, const void *d1sq, void *z,
                   cudaStream_t st)
@@ -161,7 +344,7 @@ int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const vo
         const float *p = static_cast<const float *>(data);
         InterpArgs<float> a{p, p + ndp, p + 2 * ndp, ndp, nd, (const float *)qx, (const float *)qy,
                             (const float *)alpha, (const float *)d1sq, nq, (float *)z};
-        return launch_interp_t<float, 2>(a, st);
+        return launch_interp_f32(a, st);
     }
     const double *p = static_cast<const double *>(data);
     InterpArgs<double> a{p, p + ndp, p + 2 * ndp, ndp, nd, (const double *)qx, (const double *)qy,

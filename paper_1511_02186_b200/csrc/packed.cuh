@@ -1,0 +1,84 @@
+// packed.cuh -- sm_100 packed fp32x2 arithmetic (PTX add/sub/mul/fma .rn.f32x2 ->
+// SASS FADD2 / FMUL2 / FFMA2: two IEEE round-to-nearest fp32 operations per lane per
+// issue slot) and a software exp2 on the FMA pipe used to offload part of the
+// weighting pass's ex2 work from the SFU.
+#pragma once
+
+#include <cstdint>
+
+namespace aidw {
+
+typedef unsigned long long f32x2;  // {lo, hi} fp32 pair in one 64-bit register pair
+
+__device__ __forceinline__ f32x2 pack2(float lo, float hi)
+{
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+
+__device__ __forceinline__ void unpack2(f32x2 v, float &lo, float &hi)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b)
+{
+    f32x2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b)
+{
+    f32x2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b)
+{
+    f32x2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c)
+{
+    f32x2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+__device__ __forceinline__ f32x2 splat2(float v) { return pack2(v, v); }
+
+// 2^x for x <= ~0 on the FMA pipe: x clamped to [-126, +inf), j = rint(x) via the
+// 1.5*2^23 magic constant, f = x - j in [-0.5, 0.5], 2^f by a degree-4 near-minimax
+// polynomial (max relative error 2.7e-6 in fp32 Horner form; fitted offline, see
+// tools/fit_exp2.py), exponent added as an integer: bits(2^f) + (j << 23).
+// Results below 2^-126 are not produced (the clamp): such weights are < 1e-38 of the
+// nearest point's weight (w is scaled to 1 at the nearest point) and vanish in the sums.
+__device__ __forceinline__ f32x2 exp2_poly2(f32x2 a)
+{
+    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+    float a0, a1;
+    unpack2(a, a0, a1);
+    a0 = fmaxf(a0, -126.0f);
+    a1 = fmaxf(a1, -126.0f);
+    const f32x2 x = pack2(a0, a1);
+    const f32x2 t = add2(x, splat2(kMagic));
+    const f32x2 j = sub2(t, splat2(kMagic));
+    const f32x2 f = sub2(x, j);
+    f32x2 p = fma2(splat2(0.009570101276040077f), f, splat2(0.05591785907745361f));
+    p = fma2(p, f, splat2(0.240247443318367f));
+    p = fma2(p, f, splat2(0.6931217908859253f));
+    p = fma2(p, f, splat2(0.9999992847442627f));
+    float t0, t1, p0, p1;
+    unpack2(t, t0, t1);
+    unpack2(p, p0, p1);
+    const float r0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+    const float r1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+    return pack2(r0, r1);
+}
+
+}  // namespace aidw

@@ -27,7 +27,20 @@ __global__ void bench(float *out, Clk *clk, float seed)
         for (int i = 0; i < kChains; ++i) {
             if (MODE == 0) v[i] = ex2(v[i]);                 // MUFU.EX2
             else if (MODE == 1) v[i] = lg2(v[i]);            // MUFU.LG2
-            else v[i] = fmaf(v[i], 1.0000001f, 1e-7f);       // FFMA
+            else if (MODE == 2) v[i] = fmaf(v[i], 1.0000001f, 1e-7f);  // FFMA
+            else if (MODE == 3) {                                          // FFMA2 (2 FMAs / instr)
+                if (i % 2 == 0) {
+                    float2 a = make_float2(v[i], v[i + 1]);
+                    unsigned long long r, x = *reinterpret_cast<unsigned long long *>(&a),
+                                          m = 0x3f8000013f800001ull, c = 0x33d6bf9533d6bf95ull;
+                    asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(x), "l"(m), "l"(c));
+                    float2 b = *reinterpret_cast<float2 *>(&r);
+                    v[i] = b.x; v[i + 1] = b.y;
+                }
+            } else {                                                        // MUFU + FFMA mix 1:7
+                if (i == 0) v[i] = ex2(v[i]);
+                else v[i] = fmaf(v[i], 1.0000001f, 1e-7f);
+            }
         }
     }
     unsigned long long c1 = clock64(), t1 = gtime();
@@ -60,8 +73,12 @@ int main()
     int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     float *out; Clk *clk; cudaMalloc(&out, 4); cudaMalloc(&clk, sizeof(Clk));
     double m0, m1, m2;
+    double m3, m4;
     double ex = run<0>(sms, out, clk, &m0), lg = run<1>(sms, out, clk, &m1), fm = run<2>(sms, out, clk, &m2);
+    double f2 = run<3>(sms, out, clk, &m3), mix = run<4>(sms, out, clk, &m4);
+    // modes 3/4 count values updated: mode 3 = FMAs (2 per FFMA2 instruction), mode 4 = 1 ex2 + 7 FFMA
     printf("{\"sms\": %d, \"mufu_ex2_per_clk_sm\": %.2f, \"mufu_lg2_per_clk_sm\": %.2f, \"ffma_per_clk_sm\": %.2f, "
-           "\"sm_mhz_during\": [%.0f, %.0f, %.0f]}\n", sms, ex, lg, fm, m0, m1, m2);
+           "\"ffma2_fma_per_clk_sm\": %.2f, \"ffma2_instr_per_clk_sm\": %.2f, \"mix_1ex2_7ffma_ops_per_clk_sm\": %.2f, "
+           "\"sm_mhz_during\": [%.0f, %.0f, %.0f, %.0f, %.0f]}\n", sms, ex, lg, fm, f2, f2 / 2, mix, m0, m1, m2, m3, m4);
     return 0;
 }
