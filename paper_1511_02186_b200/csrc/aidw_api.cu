@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -17,6 +18,7 @@ struct aidw_ctx {
     double area = 0.0, r_exp = 0.0;
     void *data = nullptr;            // [3][ndp] T, internal SoA
     aidw::Scratch *sc = nullptr;     // device scratch
+    aidw::FilterData filt;           // fp32 kNN filter arrays
     void *work = nullptr;            // run_host / internal d1sq scratch
     size_t work_bytes = 0;
     int64_t launches = 0;
@@ -219,6 +221,27 @@ aidw_status aidw_create(aidw_t *out, int device, aidw_dtype dt, aidw_layout lay,
         return bail(fail(h, AIDW_E_DEGENERATE_EXTENT, "study area A = %g (bbox [%g,%g]x[%g,%g])", h->area, x0,
                          x1, y0, y1));
     h->r_exp = 1.0 / (2.0 * std::sqrt((double)nd / h->area));  // Eq. 2, printed order
+
+    if (dt == AIDW_F32) {
+        // centred filter arrays for the fp32 kNN; c = bbox centre in fp32,
+        // r1 >= max |x - c_x| + |y - c_y| over the data (fp64, padded for fp32 rounding)
+        const char *env = getenv("AIDW_KNN_FILTER");
+        if (!(env && env[0] == '0')) {
+            if ((e = cudaMalloc(&h->filt.arrays, 3 * (size_t)h->ndp * sizeof(float))) != cudaSuccess) {
+                cudaGetLastError();
+                return bail(fail(h, AIDW_E_NOMEM, "cudaMalloc filter: %s", cudaGetErrorString(e)));
+            }
+            h->filt.c_x = (float)(0.5 * (x0 + x1));
+            h->filt.c_y = (float)(0.5 * (y0 + y1));
+            const double rx = std::fmax(std::fabs(x0 - h->filt.c_x), std::fabs(x1 - h->filt.c_x));
+            const double ry = std::fmax(std::fabs(y0 - h->filt.c_y), std::fabs(y1 - h->filt.c_y));
+            h->filt.r1 = (float)((rx + ry) * (1.0 + 1e-6));
+            s = launched(h, aidw::launch_center(h->data, h->ndp, nd, h->filt.c_x, h->filt.c_y, h->filt.arrays, st),
+                         "center kernel");
+            if (s != AIDW_OK) return bail(s);
+            if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return bail(cuda_fail(h, e, "center sync"));
+        }
+    }
     *out = h;
     return AIDW_OK;
 }
@@ -248,7 +271,7 @@ aidw_status aidw_knn_robs(aidw_t h, const void *qx, const void *qy, int64_t nq, 
     }
     return launched(h,
                     aidw::launch_knn((int)h->dt, k, h->data, h->ndp, qx, qy, nq, r_obs, d1sq, robs_minmax,
-                                     knn_dists, h->sc, st),
+                                     knn_dists, h->sc, &h->filt, st),
                     "knn_robs kernel");
 }
 
@@ -295,7 +318,7 @@ aidw_status aidw_interpolate(aidw_t h, const void *qx, const void *qy, int64_t n
         void *d1 = static_cast<char *>(h->work) + (size_t)nq * ts;
         s = launched(h,
                      aidw::launch_knn((int)h->dt, 1, h->data, h->ndp, qx, qy, nq, robs, d1, nullptr, nullptr,
-                                      h->sc, st),
+                                      h->sc, &h->filt, st),
                      "nearest kernel");
         if (s != AIDW_OK) return s;
         d1sq = d1;
@@ -357,10 +380,11 @@ aidw_status aidw_destroy(aidw_t h)
 {
     if (!h) return AIDW_OK;
     cudaSetDevice(h->device);
-    if (h->data || h->sc || h->work) cudaDeviceSynchronize();
+    if (h->data || h->sc || h->work || h->filt.arrays) cudaDeviceSynchronize();
     if (h->data) cudaFree(h->data);
     if (h->sc) cudaFree(h->sc);
     if (h->work) cudaFree(h->work);
+    if (h->filt.arrays) cudaFree(h->filt.arrays);
     delete h;
     return AIDW_OK;
 }

@@ -14,6 +14,8 @@ constexpr int kTileK = 1024;   // points per smem stage, kNN pass (x, y)
 constexpr int kStagesK = 4;
 constexpr int kTileW = 512;    // points per smem stage, weighting pass (x, y, z)
 constexpr int kStagesW = 4;
+constexpr int kTileKF = 512;   // points per smem stage, fp32 filtered kNN (cx, cy, pp, x, y)
+constexpr int kStagesKF = 4;
 constexpr int kPad = 1024;     // internal arrays padded to a multiple of both tiles
 
 // Device scratch owned by a handle.
@@ -27,6 +29,13 @@ struct Scratch {
     unsigned long long nonfinite;
 };
 
+// fp32 kNN filter data owned by a handle: centred coordinates and
+// |p'|^2, [3][ndp] floats padded with +inf, the centre and the bound R1.
+struct FilterData {
+    void *arrays = nullptr;
+    float c_x = 0.f, c_y = 0.f, r1 = 0.f;
+};
+
 // Each launcher returns the number of kernels it launched (>= 0) or -1 on a
 // launch error (cudaGetLastError is left set for the caller).
 int launch_prep(int dtype, int layout, const void *src, int64_t nd, int64_t ndp, void *data,
@@ -34,7 +43,10 @@ int launch_prep(int dtype, int layout, const void *src, int64_t nd, int64_t ndp,
 
 int launch_knn(int dtype, int k, const void *data, int64_t ndp, const void *qx, const void *qy,
                int64_t nq, void *r_obs, void *d1sq, void *minmax, void *dists, Scratch *sc,
-               cudaStream_t st);
+               const FilterData *filt, cudaStream_t st);
+
+int launch_center(const void *data, int64_t ndp, int64_t nd, float c_x, float c_y, void *filt,
+                  cudaStream_t st);
 
 int launch_minmax_identity(int dtype, void *minmax, cudaStream_t st);
 

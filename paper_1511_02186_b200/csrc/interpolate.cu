@@ -332,7 +332,10 @@ static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st)
     case 6: return launch_interp_f32x2<4, 0x77>(a, st);      // Q=4, 6 of 8
     case 7: return launch_interp_f32x2<4, 0x7F>(a, st);      // Q=4, 7 of 8
     case 8: return launch_interp_f32x2<4, 0x55>(a, st);      // Q=4, 4 of 8
-    default: return launch_interp_f32x2<2, 0x7>(a, st);
+    case 9: return launch_interp_f32x2<4, 0x15>(a, st);      // Q=4, 3 of 8
+    case 10: return launch_interp_f32x2<4, 0x57>(a, st);     // Q=4, 5 of 8
+    case 11: return launch_interp_f32x2<2, 0x1>(a, st);      // Q=2, 1 of 4
+    default: return launch_interp_f32x2<2, 0x5>(a, st);      // Q=2, 2 of 4 (best measured, r01)
     }
 }
 

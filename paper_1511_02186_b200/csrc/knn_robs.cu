@@ -22,6 +22,7 @@
 //    allreduce(MAX) -- no extra launch.
 #include "aidw_internal.h"
 #include "device.cuh"
+#include "packed.cuh"
 
 #include <climits>
 
@@ -75,6 +76,71 @@ __device__ __forceinline__ void topk_insert(T (&b)[K], T s)
 #pragma unroll
     for (int i = K - 1; i > 0; --i) b[i] = tmin(b[i], tmax(b[i - 1], s));
     b[0] = tmin(b[0], s);
+}
+
+// Epilogue shared by the kNN kernels: r_obs (Eq. 3, ascending sum then /k), d1sq,
+// the k distances, and the {-min, max} of r_obs (warp reduce -> one atomic per warp ->
+// last CTA publishes and resets the scratch).  Must be reached by all threads.
+template <typename T, int K, int Q>
+__device__ __forceinline__ void knn_epilogue(const KnnArgs<T> &a, T (&buf)[Q][K], const bool (&valid)[Q],
+                                             int64_t base, int k0)
+{
+    const int tid = threadIdx.x, lane = tid & 31;
+    T robs_l[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        T sum = T(0), d1 = buf[q][K - 1];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            if (i >= k0) sum = add_rn(sum, sqrt_rn(buf[q][i]));  // ascending order
+            if (i == k0) d1 = buf[q][i];
+        }
+        const T robs = div_rn(sum, (T)a.k);
+        robs_l[q] = robs;
+        const int64_t idx = base + q * kBlock;
+        if (valid[q]) {
+            a.r_obs[idx] = robs;
+            if (a.d1sq) a.d1sq[idx] = d1;
+            if (a.dists) {
+                T *o = a.dists + idx * a.k;
+#pragma unroll
+                for (int i = 0; i < K; ++i)
+                    if (i >= k0) o[i - k0] = sqrt_rn(buf[q][i]);
+            }
+        }
+    }
+
+    if (a.minmax) {
+        unsigned long long mn = ~0ull, mx = 0ull;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            unsigned long long m0, m1;
+            warp_minmax(robs_l[q], valid[q], m0, m1);
+            mn = m0 < mn ? m0 : mn;
+            mx = m1 > mx ? m1 : mx;
+        }
+        if (lane == 0) {
+            if (mn != ~0ull) atomicMin(&a.sc->mn, mn);
+            atomicMax(&a.sc->mx, mx);
+            __threadfence();
+        }
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            const unsigned ticket = atomicAdd(&a.sc->done, 1u);
+            if (ticket == gridDim.x - 1) {  // last CTA: publish and reset the scratch
+                __threadfence();
+                const unsigned long long gmn = atomicAdd(&a.sc->mn, 0ull);
+                const unsigned long long gmx = atomicAdd(&a.sc->mx, 0ull);
+                a.minmax[0] = -from_bits<T>(gmn);
+                a.minmax[1] = from_bits<T>(gmx);
+                a.sc->mn = ~0ull;
+                a.sc->mx = 0ull;
+                a.sc->done = 0u;
+                __threadfence();
+            }
+        }
+    }
 }
 
 template <typename T, int K, int Q>
@@ -168,62 +234,190 @@ __global__ void __launch_bounds__(kBlock) knn_robs_kernel(const KnnArgs<T> a)
         }
     }
 
-    // ---- epilogue: r_obs (Eq. 3), d1sq, k distances, min/max
-    T robs_l[Q];
+    knn_epilogue<T, K, Q>(a, buf, valid, base, k0);
+}
+
+
+// ---------------------------------------------------------------------------------
+// fp32 kNN with an exact-safe expanded-form filter.
+//
+// With centred coordinates p' = p - c, q' = q - c (c = bbox centre, fp32), the squared
+// distance is s' = |q'|^2 + t,  t = |p'|^2 - 2 q'.p'.  t is evaluated with two packed
+// FFMA2 per couple of points from per-point |p'|^2 (precomputed once per handle), i.e.
+// 1 FMA-pipe op + 1 compare per pair instead of 4 + 1.  A pair can only enter the top-k
+// if t <= thr_f, where thr_f is the current k-th canonical distance converted to the t
+// scale with a rigorous rounding margin (thr_of below); pairs passing the filter are
+// re-evaluated with the CANONICAL sequence (R16) on the original coordinates and the
+// insertion decision is taken on that exact value, so the selected multiset is bit-for-
+// bit the one of knn_robs_kernel / the oracle's float instantiation.
+//
+// Margin (all |.| bounds, n1 = |q'x| + |q'y|, R1 = max_p |p'x| + |p'y|, u = 2^-24):
+//   |t~ - t| <= 4u (n1 + R1)^2         (pp rounding 2u|p'|^2, two FMA roundings u|t|)
+//   canonical s >= D (1 - 4u), D the exact distance^2;  centring moves sqrt(s') by at
+//   most 2u (n1 + R1).  Hence s < thr  =>  t~ < (sqrt(thr)(1+4u) + 4u(n1+R1))^2 - |q'|^2
+//   + 8u(n1+R1)^2, evaluated in fp64 and rounded up to fp32 (factor-2 slack on each term).
+struct FilterArgs {
+    const float *cx, *cy, *pp;  // centred filter arrays, padded with +inf
+    float c_x, c_y;             // centre
+    float r1;                   // R1 bound (>= max |p'x| + |p'y|)
+};
+
+__device__ __forceinline__ float thr_of(float thr, double qq, double n1r)
+{
+    if (!(thr < pos_inf<float>())) return pos_inf<float>();
+    const double u = 0x1p-24;
+    const double r = (double)sqrtf(thr) * (1.0 + 16.0 * u) + 8.0 * u * n1r;
+    const double v = r * r - qq + 16.0 * u * n1r * n1r + 4.0 * u * qq;
+    return __double2float_ru(v);
+}
+
+template <int K, int Q>
+__global__ void __launch_bounds__(kBlock) knn_filter_kernel(const KnnArgs<float> a, const FilterArgs f)
+{
+    constexpr int TILE = kTileKF, STAGES = kStagesKF;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *scx = reinterpret_cast<float *>(smem_raw);
+    float *scy = scx + STAGES * TILE;
+    float *spp = scy + STAGES * TILE;
+    float *spx = spp + STAGES * TILE;
+    float *spy = spx + STAGES * TILE;
+    uint64_t *full = reinterpret_cast<uint64_t *>(spy + STAGES * TILE);
+    uint64_t *empty = full + STAGES;
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int ntiles = (int)(a.ndp / TILE);
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    auto issue = [&](int tile, int slot) {
+        constexpr uint32_t B = TILE * sizeof(float);
+        mbar_arrive_expect_tx(&full[slot], 5u * B);
+        const int64_t off = (int64_t)tile * TILE;
+        bulk_g2s(scx + slot * TILE, f.cx + off, B, &full[slot]);
+        bulk_g2s(scy + slot * TILE, f.cy + off, B, &full[slot]);
+        bulk_g2s(spp + slot * TILE, f.pp + off, B, &full[slot]);
+        bulk_g2s(spx + slot * TILE, a.px + off, B, &full[slot]);
+        bulk_g2s(spy + slot * TILE, a.py + off, B, &full[slot]);
+    };
+    if (tid == 0)
+        for (int s = 0; s < STAGES && s < ntiles; ++s) issue(s, s);
+
+    const int64_t base = (int64_t)blockIdx.x * (kBlock * Q) + tid;
+    float qx[Q], qy[Q], thr[Q];
+    double qq[Q], n1r[Q];
+    f32x2 A2[Q], B2[Q];
+    bool valid[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        T sum = T(0), d1 = buf[q][K - 1];
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            if (i >= k0) sum = add_rn(sum, sqrt_rn(buf[q][i]));  // ascending order
-            if (i == k0) d1 = buf[q][i];
-        }
-        const T robs = div_rn(sum, (T)a.k);
-        robs_l[q] = robs;
         const int64_t idx = base + q * kBlock;
-        if (valid[q]) {
-            a.r_obs[idx] = robs;
-            if (a.d1sq) a.d1sq[idx] = d1;
-            if (a.dists) {
-                T *o = a.dists + idx * a.k;
-#pragma unroll
-                for (int i = 0; i < K; ++i)
-                    if (i >= k0) o[i - k0] = sqrt_rn(buf[q][i]);
-            }
-        }
+        valid[q] = idx < a.nq;
+        qx[q] = valid[q] ? a.qx[idx] : 0.f;
+        qy[q] = valid[q] ? a.qy[idx] : 0.f;
+        if (valid[q] && !(isfinite(qx[q]) && isfinite(qy[q])))
+            atomicMin(&a.sc->err_idx, (long long)idx);
+        const float qcx = __fsub_rn(qx[q], f.c_x), qcy = __fsub_rn(qy[q], f.c_y);
+        A2[q] = splat2(-2.0f * qcx);
+        B2[q] = splat2(-2.0f * qcy);
+        qq[q] = (double)qcx * (double)qcx + (double)qcy * (double)qcy;
+        n1r[q] = fabs((double)qcx) + fabs((double)qcy) + (double)f.r1;
+        thr[q] = pos_inf<float>();
     }
 
-    if (a.minmax) {
-        unsigned long long mn = ~0ull, mx = 0ull;
+    float buf[Q][K];
+    const int k0 = K - a.k;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            unsigned long long m0, m1;
-            warp_minmax(robs_l[q], valid[q], m0, m1);
-            mn = m0 < mn ? m0 : mn;
-            mx = m1 > mx ? m1 : mx;
-        }
-        if (lane == 0) {
-            if (mn != ~0ull) atomicMin(&a.sc->mn, mn);
-            atomicMax(&a.sc->mx, mx);
-            __threadfence();
-        }
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            const unsigned ticket = atomicAdd(&a.sc->done, 1u);
-            if (ticket == gridDim.x - 1) {  // last CTA: publish and reset the scratch
-                __threadfence();
-                const unsigned long long gmn = atomicAdd(&a.sc->mn, 0ull);
-                const unsigned long long gmx = atomicAdd(&a.sc->mx, 0ull);
-                a.minmax[0] = -from_bits<T>(gmn);
-                a.minmax[1] = from_bits<T>(gmx);
-                a.sc->mn = ~0ull;
-                a.sc->mx = 0ull;
-                a.sc->done = 0u;
-                __threadfence();
+    for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int i = 0; i < K; ++i) buf[q][i] = (i < k0) ? -pos_inf<float>() : pos_inf<float>();
+
+    for (int t = 0; t < ntiles; ++t) {
+        const int slot = t % STAGES;
+        const uint32_t par = (uint32_t)(t / STAGES) & 1u;
+        mbar_wait(&full[slot], par);
+        const float *tcx = scx + slot * TILE, *tcy = scy + slot * TILE, *tpp = spp + slot * TILE;
+        const float *tpx = spx + slot * TILE, *tpy = spy + slot * TILE;
+#pragma unroll 2
+        for (int j = 0; j < TILE; j += 4) {
+            const float4 CX = *reinterpret_cast<const float4 *>(tcx + j);
+            const float4 CY = *reinterpret_cast<const float4 *>(tcy + j);
+            const float4 PP = *reinterpret_cast<const float4 *>(tpp + j);
+            const f32x2 cxh[2] = {pack2(CX.x, CX.y), pack2(CX.z, CX.w)};
+            const f32x2 cyh[2] = {pack2(CY.x, CY.y), pack2(CY.z, CY.w)};
+            const f32x2 pph[2] = {pack2(PP.x, PP.y), pack2(PP.z, PP.w)};
+            float tv[Q][4];
+            bool hit = false;
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const f32x2 tt = fma2(B2[q], cyh[h], fma2(A2[q], cxh[h], pph[h]));
+                    unpack2(tt, tv[q][2 * h], tv[q][2 * h + 1]);
+                    hit |= (tv[q][2 * h] <= thr[q]) | (tv[q][2 * h + 1] <= thr[q]);
+                }
+            if (__any_sync(0xffffffffu, hit)) {
+                const float4 PX = *reinterpret_cast<const float4 *>(tpx + j);
+                const float4 PY = *reinterpret_cast<const float4 *>(tpy + j);
+                const float px[4] = {PX.x, PX.y, PX.z, PX.w}, py[4] = {PY.x, PY.y, PY.z, PY.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
+                        const bool h = tv[q][e] <= thr[q];
+                        if (__any_sync(0xffffffffu, h)) {
+                            if (h) {
+                                const float s = dist_sq(qx[q], qy[q], px[e], py[e]);
+                                if (s < buf[q][K - 1]) {
+                                    topk_insert<float, K>(buf[q], s);
+                                    thr[q] = thr_of(buf[q][K - 1], qq[q], n1r[q]);
+                                }
+                            }
+                        }
+                    }
             }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (tid == 0 && t + STAGES < ntiles) {
+            mbar_wait(&empty[slot], par);
+            issue(t + STAGES, slot);
+        }
     }
+    knn_epilogue<float, K, Q>(a, buf, valid, base, k0);
+}
+
+template <int K, int Q>
+static int launch_knn_filter_t(const KnnArgs<float> &a, const FilterArgs &f, cudaStream_t st)
+{
+    const size_t smem = (size_t)5 * kStagesKF * kTileKF * sizeof(float) + 2 * kStagesKF * sizeof(uint64_t);
+    if (cudaFuncSetAttribute(knn_filter_kernel<K, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return -1;
+    const int64_t per_cta = (int64_t)kBlock * Q;
+    const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
+    knn_filter_kernel<K, Q><<<grid, kBlock, smem, st>>>(a, f);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaStream_t st)
+{
+    const int k = a.k;
+    if (k <= 1) return launch_knn_filter_t<1, 4>(a, f, st);
+    if (k <= 2) return launch_knn_filter_t<2, 4>(a, f, st);
+    if (k <= 4) return launch_knn_filter_t<4, 4>(a, f, st);
+    if (k <= 8) return launch_knn_filter_t<8, 4>(a, f, st);
+    if (k <= 10) return launch_knn_filter_t<10, 4>(a, f, st);
+    if (k <= 12) return launch_knn_filter_t<12, 4>(a, f, st);
+    if (k <= 15) return launch_knn_filter_t<15, 2>(a, f, st);
+    if (k <= 16) return launch_knn_filter_t<16, 2>(a, f, st);
+    if (k <= 24) return launch_knn_filter_t<24, 2>(a, f, st);
+    return launch_knn_filter_t<32, 2>(a, f, st);
 }
 
 template <typename T> __global__ void minmax_identity_kernel(T *mm)
@@ -263,12 +457,17 @@ static int dispatch_k(const KnnArgs<T> &a, cudaStream_t st)
 
 int launch_knn(int dtype, int k, const void *data, int64_t ndp, const void *qx, const void *qy,
                int64_t nq, void *r_obs, void *d1sq, void *minmax, void *dists, Scratch *sc,
-               cudaStream_t st)
+               const FilterData *filt, cudaStream_t st)
 {
     if (dtype == 0) {
         const float *p = static_cast<const float *>(data);
         KnnArgs<float> a{p, p + ndp, ndp, (const float *)qx, (const float *)qy, nq, k,
                          (float *)r_obs, (float *)d1sq, (float *)minmax, (float *)dists, sc};
+        if (filt && filt->arrays) {
+            const float *c = static_cast<const float *>(filt->arrays);
+            FilterArgs f{c, c + ndp, c + 2 * ndp, filt->c_x, filt->c_y, filt->r1};
+            return dispatch_filter_k(a, f, st);
+        }
         return dispatch_k(a, st);
     }
     const double *p = static_cast<const double *>(data);

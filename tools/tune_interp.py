@@ -12,7 +12,7 @@ import torch
 import datagen
 import paper_1511_02186_b200 as P
 
-nq = int(sys.argv[2]) if len(sys.argv) > 2 else 1024000
+nq = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 1024000
 x, y, z = datagen.make_data("C4")
 qx, qy = datagen.make_queries("C4", nq=nq)
 eng = P.AIDW(x, y, z)
