@@ -36,11 +36,29 @@ NQ_PER_GPU = 1000 * datagen.K_SIZE
 K_NN = 10
 SEED = 1004  # C4
 METRIC = "AIDW interpolated points/sec (fp32; 1M data x 1M queries per GPU, k=10, GLOBAL R bounds)"
-SFU_PER_PAIR = 2        # lg2 + ex2 per weighting pair
-MUFU_PER_CLK_SM = 16    # B200 SFU lanes per SM per clock (measured: profiles/)
-FP32_PER_CLK_SM = 128
-KNN_FP32_PER_PAIR = 4
+# Roofline model of the weighting pass.  Per (query, data point) pair
+# the method needs 7 FP32 operations (s: 2 sub + mul + fma; exponent fma; two sums)
+# and 2 transcendentals (log2, exp2).  A transcendental costs 1 SFU op, or 8 FMA-pipe
+# ops when evaluated as a polynomial; the best split of the work over the two pipes
+# gives the bound.  Pipe rates: profiles/r01_pipe_peaks.json (measured on B200).
+WEIGHT_FP32_PER_PAIR = 7
+TRANSC_PER_PAIR = 2
+POLY_FMA_PER_TRANSC = 8
+MUFU_PER_CLK_SM = 15.96   # measured MUFU.EX2/LG2 per SM per clock
+FMA_PER_CLK_SM = 123.2    # measured FFMA2 (packed) FMA ops per SM per clock
+KNN_FP32_PER_PAIR = 4     # canonical kNN distance (2 sub, mul, fma) -- SIMT FP32 bound
 N_SM = 148
+
+
+def weight_clk_per_pair():
+    """min over the SFU fraction of max(FMA-pipe time, SFU time), clocks per pair per SM."""
+    best = None
+    for i in range(0, 2001):
+        f = TRANSC_PER_PAIR * i / 2000.0  # transcendentals moved to the FMA pipe
+        t = max((WEIGHT_FP32_PER_PAIR + POLY_FMA_PER_TRANSC * f) / FMA_PER_CLK_SM,
+                (TRANSC_PER_PAIR - f) / MUFU_PER_CLK_SM)
+        best = t if best is None else min(best, t)
+    return best
 
 
 def peaks():
@@ -316,10 +334,11 @@ def main():
     ar_ms = float(per[:, 1].mean())
     alpha_ms = float(per[:, 2].mean())
     interp_ms = float(per[:, 3].mean())
-    # dominant kernel: the weighting pass, SFU-bound (2 MUFU per pair)
+    # dominant kernel: the weighting pass, bound by the SFU + FMA pipes together
     interp_rate = pairs / (interp_ms / 1e3)
-    sfu_peak_pairs = N_SM * MUFU_PER_CLK_SM / SFU_PER_PAIR * f_max
-    path_clk_per_pair = (KNN_FP32_PER_PAIR / FP32_PER_CLK_SM + SFU_PER_PAIR / MUFU_PER_CLK_SM) / 1.0
+    w_clk = weight_clk_per_pair()
+    sfu_peak_pairs = N_SM * f_max / w_clk
+    path_clk_per_pair = KNN_FP32_PER_PAIR / FMA_PER_CLK_SM + w_clk
     path_peak_pairs = N_SM * f_max / path_clk_per_pair
     traffic = None
     try:
@@ -356,10 +375,13 @@ def main():
             "bound": "alu", "kernel": "interp_kernel (S5 weighting pass)",
             "achieved": interp_rate / 1e9, "peak": sfu_peak_pairs / 1e9, "unit": "Gpair/s",
             "frac": interp_rate / sfu_peak_pairs, "traffic": traffic,
-            "peak_basis": f"{N_SM} SM x {MUFU_PER_CLK_SM} MUFU/clk / {SFU_PER_PAIR} MUFU per pair x "
-                          f"{f_max / 1e6:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
+            "peak_basis": f"{N_SM} SM x {f_max / 1e6:.0f} MHz / {w_clk:.4f} clk per pair: 7 FP32 + 2 "
+                          f"transcendentals per pair split optimally between SFU ({MUFU_PER_CLK_SM}/clk) and "
+                          f"FMA pipe ({FMA_PER_CLK_SM}/clk, 8 ops per polynomial transcendental); measured pipe "
+                          f"rates profiles/r01_pipe_peaks.json; sm_max_mhz from MEASURED_PEAKS.json",
+            "sfu_only_peak": N_SM * MUFU_PER_CLK_SM / TRANSC_PER_PAIR * f_max / 1e9,
             "path_frac": (pairs / (ms / 1e3)) / path_peak_pairs,
-            "path_peak_basis": "kNN 4 FP32/pair @128/clk + weighting 2 MUFU/pair @16/clk, per SM",
+            "path_peak_basis": "kNN 4 FP32/pair on the FMA pipe + the weighting bound above, per SM",
             "frac_at_measured_clock": (interp_rate / sfu_peak_pairs) * (f_max / (clocks["sm_mhz"] * 1e6))
             if clocks.get("sm_mhz") else None,
         },

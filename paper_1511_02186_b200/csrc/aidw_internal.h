@@ -15,7 +15,7 @@ constexpr int kStagesK = 4;
 constexpr int kTileW = 512;    // points per smem stage, weighting pass (x, y, z)
 constexpr int kStagesW = 4;
 constexpr int kTileKF = 512;   // points per smem stage, fp32 filtered kNN (cx, cy, pp, x, y)
-constexpr int kStagesKF = 4;
+constexpr int kStagesKF = 3;
 constexpr int kPad = 1024;     // internal arrays padded to a multiple of both tiles
 
 // Device scratch owned by a handle.

@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kBlock) interp_f32x2_kernel(const InterpArgs<f
         const float *tz = sz + slot * TILE;
         f32x2 sw[Q], swz[Q];
 #pragma unroll
-        for (int q = 0; q < Q; ++q) sw[q] = swz[q] = 0ull;
+        for (int q = 0; q < Q; ++q) sw[q] = swz[q] = make_float2(0.f, 0.f);
 #pragma unroll 2
         for (int j = 0; j < TILE; j += 4) {
             const float4 X = *reinterpret_cast<const float4 *>(tx + j);

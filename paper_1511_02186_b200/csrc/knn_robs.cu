@@ -25,6 +25,7 @@
 #include "packed.cuh"
 
 #include <climits>
+#include <cstdlib>
 
 namespace aidw {
 
@@ -262,16 +263,20 @@ struct FilterArgs {
     float r1;                   // R1 bound (>= max |p'x| + |p'y|)
 };
 
-__device__ __forceinline__ float thr_of(float thr, double qq, double n1r)
+// thr_of: the filter threshold for the canonical k-th distance thr (see margin above),
+// in fp32 with every rounding error covered: sqrt rounded up, (1 + 2^-20) and 2^-21
+// slack terms absorb the <= 3 roundings of the remaining fp32 operations.
+//   qq = |q'|^2 (rounded up), m = 4u(n1+R1) (centring), E = 16u(n1+R1)^2 + 4u qq.
+__device__ __forceinline__ float thr_of(float thr, float qq, float m, float E)
 {
     if (!(thr < pos_inf<float>())) return pos_inf<float>();
-    const double u = 0x1p-24;
-    const double r = (double)sqrtf(thr) * (1.0 + 16.0 * u) + 8.0 * u * n1r;
-    const double v = r * r - qq + 16.0 * u * n1r * n1r + 4.0 * u * qq;
-    return __double2float_ru(v);
+    const float r = __fmaf_ru(__fsqrt_ru(thr), 1.0f + 0x1p-20f, m);
+    const float r2 = __fmul_ru(r, r);
+    const float v = __fadd_ru(__fadd_ru(r2, -qq), E);
+    return __fmaf_ru(0x1p-21f, r2 + qq + E, v);
 }
 
-template <int K, int Q>
+template <int K, int Q, int G>
 __global__ void __launch_bounds__(kBlock) knn_filter_kernel(const KnnArgs<float> a, const FilterArgs f)
 {
     constexpr int TILE = kTileKF, STAGES = kStagesKF;
@@ -310,8 +315,7 @@ __global__ void __launch_bounds__(kBlock) knn_filter_kernel(const KnnArgs<float>
         for (int s = 0; s < STAGES && s < ntiles; ++s) issue(s, s);
 
     const int64_t base = (int64_t)blockIdx.x * (kBlock * Q) + tid;
-    float qx[Q], qy[Q], thr[Q];
-    double qq[Q], n1r[Q];
+    float qx[Q], qy[Q], thr[Q], qqf[Q], mf[Q], Ef[Q];
     f32x2 A2[Q], B2[Q];
     bool valid[Q];
 #pragma unroll
@@ -325,9 +329,15 @@ __global__ void __launch_bounds__(kBlock) knn_filter_kernel(const KnnArgs<float>
         const float qcx = __fsub_rn(qx[q], f.c_x), qcy = __fsub_rn(qy[q], f.c_y);
         A2[q] = splat2(-2.0f * qcx);
         B2[q] = splat2(-2.0f * qcy);
-        qq[q] = (double)qcx * (double)qcx + (double)qcy * (double)qcy;
-        n1r[q] = fabs((double)qcx) + fabs((double)qcy) + (double)f.r1;
         thr[q] = pos_inf<float>();
+        {   // margin terms (fp64, rounded up to fp32)
+            const double u = 0x1p-24;
+            const double qq = (double)qcx * (double)qcx + (double)qcy * (double)qcy;
+            const double n1r = fabs((double)qcx) + fabs((double)qcy) + (double)f.r1;
+            qqf[q] = __double2float_ru(qq);
+            mf[q] = __double2float_ru(8.0 * u * n1r);
+            Ef[q] = __double2float_ru(16.0 * u * n1r * n1r + 4.0 * u * qq + 2.0 * u * qq);
+        }
     }
 
     float buf[Q][K];
@@ -343,43 +353,58 @@ __global__ void __launch_bounds__(kBlock) knn_filter_kernel(const KnnArgs<float>
         mbar_wait(&full[slot], par);
         const float *tcx = scx + slot * TILE, *tcy = scy + slot * TILE, *tpp = spp + slot * TILE;
         const float *tpx = spx + slot * TILE, *tpy = spy + slot * TILE;
-#pragma unroll 2
-        for (int j = 0; j < TILE; j += 4) {
-            const float4 CX = *reinterpret_cast<const float4 *>(tcx + j);
-            const float4 CY = *reinterpret_cast<const float4 *>(tcy + j);
-            const float4 PP = *reinterpret_cast<const float4 *>(tpp + j);
-            const f32x2 cxh[2] = {pack2(CX.x, CX.y), pack2(CX.z, CX.w)};
-            const f32x2 cyh[2] = {pack2(CY.x, CY.y), pack2(CY.z, CY.w)};
-            const f32x2 pph[2] = {pack2(PP.x, PP.y), pack2(PP.z, PP.w)};
-            float tv[Q][4];
+#pragma unroll 1
+        for (int j = 0; j < TILE; j += G) {
+            // G points per warp vote; per query a min-tree of the G filter values
+            float cxv[G], cyv[G], ppv[G];
+#pragma unroll
+            for (int g = 0; g < G; g += 4) {
+                const float4 CX = *reinterpret_cast<const float4 *>(tcx + j + g);
+                const float4 CY = *reinterpret_cast<const float4 *>(tcy + j + g);
+                const float4 PP = *reinterpret_cast<const float4 *>(tpp + j + g);
+                cxv[g] = CX.x; cxv[g + 1] = CX.y; cxv[g + 2] = CX.z; cxv[g + 3] = CX.w;
+                cyv[g] = CY.x; cyv[g + 1] = CY.y; cyv[g + 2] = CY.z; cyv[g + 3] = CY.w;
+                ppv[g] = PP.x; ppv[g + 1] = PP.y; ppv[g + 2] = PP.z; ppv[g + 3] = PP.w;
+            }
             bool hit = false;
 #pragma unroll
-            for (int q = 0; q < Q; ++q)
+            for (int q = 0; q < Q; ++q) {
+                float tv[G];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const f32x2 tt = fma2(B2[q], cyh[h], fma2(A2[q], cxh[h], pph[h]));
-                    unpack2(tt, tv[q][2 * h], tv[q][2 * h + 1]);
-                    hit |= (tv[q][2 * h] <= thr[q]) | (tv[q][2 * h + 1] <= thr[q]);
+                for (int h = 0; h < G / 2; ++h) {
+                    const f32x2 tt = fma2(B2[q], pack2(cyv[2 * h], cyv[2 * h + 1]),
+                                          fma2(A2[q], pack2(cxv[2 * h], cxv[2 * h + 1]),
+                                               pack2(ppv[2 * h], ppv[2 * h + 1])));
+                    unpack2(tt, tv[2 * h], tv[2 * h + 1]);
                 }
-            if (__any_sync(0xffffffffu, hit)) {
-                const float4 PX = *reinterpret_cast<const float4 *>(tpx + j);
-                const float4 PY = *reinterpret_cast<const float4 *>(tpy + j);
-                const float px[4] = {PX.x, PX.y, PX.z, PX.w}, py[4] = {PY.x, PY.y, PY.z, PY.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
+                for (int w = 1; w < G; w *= 2)
+#pragma unroll
+                    for (int i = 0; i + w < G; i += 2 * w) tv[i] = fminf(tv[i], tv[i + w]);
+                hit |= tv[0] <= thr[q];
+            }
+            if (__any_sync(0xffffffffu, hit)) {
+                // rare path (a few % of groups): re-derive each pair's filter value from
+                // smem (same RN fma as FFMA2), then the canonical distance on the original
+                // coordinates decides the insertion
+#pragma unroll 1
+                for (int e = j; e < j + G; ++e) {
+                    const float ce = tcx[e], de = tcy[e], pe = tpp[e];
 #pragma unroll
                     for (int q = 0; q < Q; ++q) {
-                        const bool h = tv[q][e] <= thr[q];
+                        const float tq = __fmaf_rn(B2[q].x, de, __fmaf_rn(A2[q].x, ce, pe));
+                        const bool h = tq <= thr[q];
                         if (__any_sync(0xffffffffu, h)) {
                             if (h) {
-                                const float s = dist_sq(qx[q], qy[q], px[e], py[e]);
+                                const float s = dist_sq(qx[q], qy[q], tpx[e], tpy[e]);
                                 if (s < buf[q][K - 1]) {
                                     topk_insert<float, K>(buf[q], s);
-                                    thr[q] = thr_of(buf[q][K - 1], qq[q], n1r[q]);
+                                    thr[q] = thr_of(buf[q][K - 1], qqf[q], mf[q], Ef[q]);
                                 }
                             }
                         }
                     }
+                }
             }
         }
         __syncwarp();
@@ -392,28 +417,212 @@ __global__ void __launch_bounds__(kBlock) knn_filter_kernel(const KnnArgs<float>
     knn_epilogue<float, K, Q>(a, buf, valid, base, k0);
 }
 
-template <int K, int Q>
+template <int K, int Q, int G = 8>
 static int launch_knn_filter_t(const KnnArgs<float> &a, const FilterArgs &f, cudaStream_t st)
 {
     const size_t smem = (size_t)5 * kStagesKF * kTileKF * sizeof(float) + 2 * kStagesKF * sizeof(uint64_t);
-    if (cudaFuncSetAttribute(knn_filter_kernel<K, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (cudaFuncSetAttribute(knn_filter_kernel<K, Q, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return -1;
     const int64_t per_cta = (int64_t)kBlock * Q;
     const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
-    knn_filter_kernel<K, Q><<<grid, kBlock, smem, st>>>(a, f);
+    knn_filter_kernel<K, Q, G><<<grid, kBlock, smem, st>>>(a, f);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// v2 of the filtered fp32 kNN: software-pipelined (the next group's smem loads are
+// issued right after the current group's filter values are formed, so they overlap
+// the warp vote), and a bitmask rare path that re-checks only the passing pairs.
+// The insertion decision is unchanged (canonical s < k-th), so results are identical.
+template <int K, int Q, int G>
+__global__ void __launch_bounds__(kBlock) knn_filter2_kernel(const KnnArgs<float> a, const FilterArgs f)
+{
+    constexpr int TILE = kTileKF, STAGES = kStagesKF;
+    static_assert(G % 4 == 0 && G <= 32 && TILE % G == 0, "group size");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *scx = reinterpret_cast<float *>(smem_raw);
+    float *scy = scx + STAGES * TILE;
+    float *spp = scy + STAGES * TILE;
+    float *spx = spp + STAGES * TILE;
+    float *spy = spx + STAGES * TILE;
+    uint64_t *full = reinterpret_cast<uint64_t *>(spy + STAGES * TILE);
+    uint64_t *empty = full + STAGES;
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int ntiles = (int)(a.ndp / TILE);
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    auto issue = [&](int tile, int slot) {
+        constexpr uint32_t B = TILE * sizeof(float);
+        mbar_arrive_expect_tx(&full[slot], 5u * B);
+        const int64_t off = (int64_t)tile * TILE;
+        bulk_g2s(scx + slot * TILE, f.cx + off, B, &full[slot]);
+        bulk_g2s(scy + slot * TILE, f.cy + off, B, &full[slot]);
+        bulk_g2s(spp + slot * TILE, f.pp + off, B, &full[slot]);
+        bulk_g2s(spx + slot * TILE, a.px + off, B, &full[slot]);
+        bulk_g2s(spy + slot * TILE, a.py + off, B, &full[slot]);
+    };
+    if (tid == 0)
+        for (int s = 0; s < STAGES && s < ntiles; ++s) issue(s, s);
+
+    const int64_t base = (int64_t)blockIdx.x * (kBlock * Q) + tid;
+    float qx[Q], qy[Q], thr[Q], qqf[Q], mf[Q], Ef[Q], A[Q], B[Q];
+    bool valid[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int64_t idx = base + q * kBlock;
+        valid[q] = idx < a.nq;
+        qx[q] = valid[q] ? a.qx[idx] : 0.f;
+        qy[q] = valid[q] ? a.qy[idx] : 0.f;
+        if (valid[q] && !(isfinite(qx[q]) && isfinite(qy[q])))
+            atomicMin(&a.sc->err_idx, (long long)idx);
+        const float qcx = __fsub_rn(qx[q], f.c_x), qcy = __fsub_rn(qy[q], f.c_y);
+        A[q] = -2.0f * qcx;
+        B[q] = -2.0f * qcy;
+        thr[q] = pos_inf<float>();
+        const double u = 0x1p-24;
+        const double qq = (double)qcx * (double)qcx + (double)qcy * (double)qcy;
+        const double n1r = fabs((double)qcx) + fabs((double)qcy) + (double)f.r1;
+        qqf[q] = __double2float_ru(qq);
+        mf[q] = __double2float_ru(8.0 * u * n1r);
+        Ef[q] = __double2float_ru(16.0 * u * n1r * n1r + 6.0 * u * qq);
+    }
+
+    float buf[Q][K];
+    const int k0 = K - a.k;
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int i = 0; i < K; ++i) buf[q][i] = (i < k0) ? -pos_inf<float>() : pos_inf<float>();
+
+    for (int t = 0; t < ntiles; ++t) {
+        const int slot = t % STAGES;
+        const uint32_t par = (uint32_t)(t / STAGES) & 1u;
+        mbar_wait(&full[slot], par);
+        const float *tcx = scx + slot * TILE, *tcy = scy + slot * TILE, *tpp = spp + slot * TILE;
+        const float *tpx = spx + slot * TILE, *tpy = spy + slot * TILE;
+
+        float cxv[G], cyv[G], ppv[G];
+        auto load = [&](int j) {
+#pragma unroll
+            for (int g = 0; g < G; g += 4) {
+                const float4 CX = *reinterpret_cast<const float4 *>(tcx + j + g);
+                const float4 CY = *reinterpret_cast<const float4 *>(tcy + j + g);
+                const float4 PP = *reinterpret_cast<const float4 *>(tpp + j + g);
+                cxv[g] = CX.x; cxv[g + 1] = CX.y; cxv[g + 2] = CX.z; cxv[g + 3] = CX.w;
+                cyv[g] = CY.x; cyv[g + 1] = CY.y; cyv[g + 2] = CY.z; cyv[g + 3] = CY.w;
+                ppv[g] = PP.x; ppv[g + 1] = PP.y; ppv[g + 2] = PP.z; ppv[g + 3] = PP.w;
+            }
+        };
+        load(0);
+#pragma unroll 1
+        for (int j = 0; j < TILE; j += G) {
+            float tv[Q][G];
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+                for (int h = 0; h < G / 2; ++h) {
+                    const f32x2 tt = fma2(splat2(B[q]), pack2(cyv[2 * h], cyv[2 * h + 1]),
+                                          fma2(splat2(A[q]), pack2(cxv[2 * h], cxv[2 * h + 1]),
+                                               pack2(ppv[2 * h], ppv[2 * h + 1])));
+                    tv[q][2 * h] = tt.x;
+                    tv[q][2 * h + 1] = tt.y;
+                }
+            load(j + G < TILE ? j + G : j);  // next group's loads overlap the vote below
+            bool hit = false;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                float m[G];
+#pragma unroll
+                for (int i = 0; i < G; ++i) m[i] = tv[q][i];
+#pragma unroll
+                for (int w = 1; w < G; w *= 2)
+#pragma unroll
+                    for (int i = 0; i + w < G; i += 2 * w) m[i] = fminf(m[i], m[i + w]);
+                hit |= m[0] <= thr[q];
+            }
+            if (__any_sync(0xffffffffu, hit)) {
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    unsigned mask = 0;
+#pragma unroll
+                    for (int e = 0; e < G; ++e) mask |= (tv[q][e] <= thr[q]) ? (1u << e) : 0u;
+                    while (__any_sync(0xffffffffu, mask != 0)) {
+                        if (mask) {
+                            const int e = __ffs(mask) - 1;
+                            mask &= mask - 1;
+                            const float s = dist_sq(qx[q], qy[q], tpx[j + e], tpy[j + e]);
+                            if (s < buf[q][K - 1]) {
+                                topk_insert<float, K>(buf[q], s);
+                                thr[q] = thr_of(buf[q][K - 1], qqf[q], mf[q], Ef[q]);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (tid == 0 && t + STAGES < ntiles) {
+            mbar_wait(&empty[slot], par);
+            issue(t + STAGES, slot);
+        }
+    }
+    knn_epilogue<float, K, Q>(a, buf, valid, base, k0);
+}
+
+template <int K, int Q, int G = 8>
+static int launch_knn_filter2_t(const KnnArgs<float> &a, const FilterArgs &f, cudaStream_t st)
+{
+    const size_t smem = (size_t)5 * kStagesKF * kTileKF * sizeof(float) + 2 * kStagesKF * sizeof(uint64_t);
+    if (cudaFuncSetAttribute(knn_filter2_kernel<K, Q, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(knn_filter2_kernel<K, Q, G>, cudaFuncAttributePreferredSharedMemoryCarveout, 100) !=
+            cudaSuccess)
+        return -1;
+    const int64_t per_cta = (int64_t)kBlock * Q;
+    const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
+    knn_filter2_kernel<K, Q, G><<<grid, kBlock, smem, st>>>(a, f);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+static int knn_variant()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("AIDW_KNN_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
 }
 
 static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaStream_t st)
 {
     const int k = a.k;
-    if (k <= 1) return launch_knn_filter_t<1, 4>(a, f, st);
-    if (k <= 2) return launch_knn_filter_t<2, 4>(a, f, st);
-    if (k <= 4) return launch_knn_filter_t<4, 4>(a, f, st);
-    if (k <= 8) return launch_knn_filter_t<8, 4>(a, f, st);
-    if (k <= 10) return launch_knn_filter_t<10, 4>(a, f, st);
-    if (k <= 12) return launch_knn_filter_t<12, 4>(a, f, st);
+    if (k <= 10 && k > 8) {
+        switch (knn_variant()) {
+        case 1: return launch_knn_filter_t<10, 2, 8>(a, f, st);   // v1
+        case 2: return launch_knn_filter2_t<10, 4, 8>(a, f, st);
+        case 3: return launch_knn_filter2_t<10, 2, 16>(a, f, st);
+        case 4: return launch_knn_filter2_t<10, 3, 8>(a, f, st);
+        case 5: return launch_knn_filter2_t<10, 2, 4>(a, f, st);
+        default: break;
+        }
+    }
+    if (k <= 1) return launch_knn_filter_t<1, 2>(a, f, st);
+    if (k <= 2) return launch_knn_filter_t<2, 2>(a, f, st);
+    if (k <= 4) return launch_knn_filter_t<4, 2>(a, f, st);
+    if (k <= 8) return launch_knn_filter_t<8, 2>(a, f, st);
+    if (k <= 10) return launch_knn_filter2_t<10, 2>(a, f, st);
+    if (k <= 12) return launch_knn_filter_t<12, 2>(a, f, st);
     if (k <= 15) return launch_knn_filter_t<15, 2>(a, f, st);
     if (k <= 16) return launch_knn_filter_t<16, 2>(a, f, st);
     if (k <= 24) return launch_knn_filter_t<24, 2>(a, f, st);

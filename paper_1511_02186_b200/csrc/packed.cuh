@@ -8,49 +8,17 @@
 
 namespace aidw {
 
-typedef unsigned long long f32x2;  // {lo, hi} fp32 pair in one 64-bit register pair
+typedef float2 f32x2;  // {lo, hi} fp32 pair in one 64-bit register pair
 
-__device__ __forceinline__ f32x2 pack2(float lo, float hi)
-{
-    f32x2 r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-    return r;
-}
-
-__device__ __forceinline__ void unpack2(f32x2 v, float &lo, float &hi)
-{
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-
-__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b)
-{
-    f32x2 r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-
-__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b)
-{
-    f32x2 r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-
-__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b)
-{
-    f32x2 r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-
-__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c)
-{
-    f32x2 r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-
-__device__ __forceinline__ f32x2 splat2(float v) { return pack2(v, v); }
+// CUDA 12.9 sm_100 builtins (crt/sm_100_rt.h): visible to the optimiser and the
+// scheduler, unlike inline PTX.
+__device__ __forceinline__ f32x2 pack2(float lo, float hi) { return make_float2(lo, hi); }
+__device__ __forceinline__ void unpack2(f32x2 v, float &lo, float &hi) { lo = v.x; hi = v.y; }
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ f32x2 splat2(float v) { return make_float2(v, v); }
 
 // 2^x for x <= ~0 on the FMA pipe: x clamped to [-126, +inf), j = rint(x) via the
 // 1.5*2^23 magic constant, f = x - j in [-0.5, 0.5], 2^f by a degree-4 near-minimax
