@@ -202,6 +202,9 @@ def main():
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no baselines, no flush)")
     ap.add_argument("--nq", type=int, default=NQ_PER_GPU, help="queries per GPU (default C4)")
     ap.add_argument("--ref-queries-per-step", type=int, default=0)
+    ap.add_argument("--mode", default="global", choices=["global", "fixed"],
+                    help="global: 3 kernels + allreduce (north star, default); fixed: R bounds (0, 2), "
+                         "one fused kernel per step (N1)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -216,17 +219,24 @@ def main():
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; AIDW_DIST_BACKEND=gloo + more ranks than GPUs is a logic
+    # test mode (ranks share a device), never a bench configuration
+    backend = os.environ.get("AIDW_DIST_BACKEND", "nccl")
+    gpu = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         group = dist.group.WORLD
 
     nq = args.nq
     x, y, z = datagen.make_data({"nd": ND, "data": "uniform"}, seed=SEED)
     qx_np, qy_np = datagen.uniform_points(SEED, nq, datagen.S_QX, datagen.S_QY, offset=rank * nq)
-    eng = P.AIDW(x, y, z, dtype=torch.float32, device=local)
+    eng = P.AIDW(x, y, z, dtype=torch.float32, device=gpu)
     qx = torch.as_tensor(qx_np, dtype=torch.float32, device=dev)
     qy = torch.as_tensor(qy_np, dtype=torch.float32, device=dev)
     st = torch.cuda.current_stream(dev)
@@ -239,7 +249,15 @@ def main():
     mm = torch.empty(2, dtype=torch.float32, device=dev)
     lv = datagen.ALPHA_LEVELS
 
+    def step_fixed(ev=None):
+        if ev: ev[0].record(st)
+        P.aidw_run_fixed(eng.h, qx, qy, K_NN, lv, 0.0, 2.0, P.NORMALIZED, zo, None, None, st)
+        for i in range(1, 5):
+            if ev: ev[i].record(st)
+
     def step(ev=None):
+        if args.mode == "fixed":
+            return step_fixed(ev)
         if ev: ev[0].record(st)
         P.aidw_knn_robs(eng.h, qx, qy, K_NN, r_obs, d1, mm, None, st)
         if ev: ev[1].record(st)
@@ -266,7 +284,7 @@ def main():
     if group is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(gpu) as clk:
         for i in range(args.steps):
             flush.fill_(i & 0xFF)  # L2 flush (256 MiB write) outside the step's events
             step(evs[i])
@@ -302,7 +320,12 @@ def main():
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            if group is None:
+            if args.mode == "fixed":
+                dx = hx.to(dev, non_blocking=True)
+                dy = hy.to(dev, non_blocking=True)
+                zz = eng.run_fixed(dx, dy, K_NN, lv, 0.0, 2.0)
+                hz.copy_(zz, non_blocking=True)
+            elif group is None:
                 eng.run_host(hx, hy, K_NN, lv, P.GLOBAL, out=hz)  # C ABI aidw_run_host
             else:
                 dx = hx.to(dev, non_blocking=True)
@@ -347,6 +370,17 @@ def main():
     except Exception:
         pass
     value = nq * world / (ms / 1e3)
+    if args.mode == "fixed":  # one fused kernel per step: its roofline is the path bound
+        fused_rate = pairs / (knn_ms / 1e3)
+        roof = {"bound": "alu", "kernel": "fused_fixed_kernel (N1: S1..S5 in one launch)",
+                "achieved": fused_rate / 1e9, "peak": path_peak_pairs / 1e9, "unit": "Gpair/s",
+                "frac": fused_rate / path_peak_pairs, "traffic": None,
+                "peak_basis": "kNN 4 FP32/pair on the FMA pipe + the pipe-balanced weighting bound "
+                              f"({w_clk:.4f} clk/pair), {N_SM} SM x {f_max / 1e6:.0f} MHz"}
+        phases = {"fused": knn_ms}
+    else:
+        roof = None
+        phases = {"knn_robs": knn_ms, "allreduce": ar_ms, "alpha": alpha_ms, "interpolate": interp_ms}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         rate, cores, sample = cpu_oracle_rate(x, y, z, qx_np, qy_np)
@@ -365,13 +399,15 @@ def main():
         "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": workload_name(world), "nd": ND, "nq_per_gpu": nq, "nq_total": nq * world,
-                   "k": K_NN, "alpha_levels": list(lv), "rbounds": "global", "mu": "normalized",
+                   "k": K_NN, "alpha_levels": list(lv),
+                   "rbounds": "global" if args.mode == "global" else "fixed (0, 2), fused single kernel",
+                   "mu": "normalized",
                    "l2": "flushed between steps (256 MiB write outside the timed events)",
                    "parallelism": f"query-sharded x{world}, data replicated"},
         "pair_evals_per_s": 2 * pairs * world / (ms / 1e3),
         "aidw_pairs_per_s": pairs * world / (ms / 1e3),
-        "phases_ms": {"knn_robs": knn_ms, "allreduce": ar_ms, "alpha": alpha_ms, "interpolate": interp_ms},
-        "roofline": {
+        "phases_ms": phases,
+        "roofline": roof or {
             "bound": "alu", "kernel": "interp_kernel (S5 weighting pass)",
             "achieved": interp_rate / 1e9, "peak": sfu_peak_pairs / 1e9, "unit": "Gpair/s",
             "frac": interp_rate / sfu_peak_pairs, "traffic": traffic,

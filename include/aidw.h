@@ -166,6 +166,29 @@ AIDW_API aidw_status aidw_interpolate(aidw_t h, const void *qx, const void *qy, 
                              const void *alpha, const void *d1sq, void *z_out, void *stream);
 
 /*
+ * aidw_run_fixed -- N1: S1..S5 with FIXED bounds in ONE launch -- the
+ * paper's per-thread structure (kNN -> r_obs -> R -> mu -> alpha -> Eq. 1 in one kernel,
+ * PAPER.md:407-438).  With caller-given R_min < R_max (paper default 0.0 / 2.0,
+ * PAPER.md:221-223) no phase barrier is needed.  fp32 handles run one fused kernel; fp64
+ * handles run the three stage kernels.  Results equal aidw_knn_robs + aidw_alpha(FIXED)
+ * + aidw_interpolate.
+ *   qx, qy     : device T[nq];  z_out : device T[nq] out
+ *   r_obs_out, alpha_out : device T[nq] out, nullable (diagnostics)
+ */
+AIDW_API aidw_status aidw_run_fixed(aidw_t h, const void *qx, const void *qy, int64_t nq, int k,
+                                    const double *alpha_lv, double r_min, double r_max, aidw_muform mf,
+                                    void *z_out, void *r_obs_out, void *alpha_out, void *stream);
+
+/*
+ * aidw_idw -- N2: standard IDW (Eq. 1 with a user-specified constant power alpha for all
+ * queries) on the same weighting kernel: one k = 1 pass for the
+ * nearest distance (weight scaling, coincidence), then the weighting pass.
+ *   alpha : finite, > 0;  qx, qy : device T[nq];  z_out : device T[nq] out
+ */
+AIDW_API aidw_status aidw_idw(aidw_t h, const void *qx, const void *qy, int64_t nq, double alpha,
+                              void *z_out, void *stream);
+
+/*
  * aidw_run_host -- the whole single-GPU path from HOST buffers: H2D of the
  * queries, knn_robs, (GLOBAL: local bounds = the job's bounds), alpha,
  * interpolate, D2H of Z; synchronises `stream` and reports deferred errors.

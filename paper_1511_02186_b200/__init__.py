@@ -23,7 +23,7 @@ from ._build import build as build_extension
 __all__ = [
     "AIDW", "AidwError", "lib", "build_extension",
     "aidw_create", "aidw_knn_robs", "aidw_alpha", "aidw_interpolate", "aidw_destroy",
-    "aidw_run_host", "aidw_check", "GLOBAL", "FIXED", "NORMALIZED", "PRINTED",
+    "aidw_run_host", "aidw_check", "aidw_run_fixed", "aidw_idw", "GLOBAL", "FIXED", "NORMALIZED", "PRINTED",
 ]
 
 F32, F64 = 0, 1
@@ -43,7 +43,7 @@ _STATUS = {
 EXPORTS = (
     "aidw_abi_version", "aidw_status_string", "aidw_last_error", "aidw_create", "aidw_nd",
     "aidw_area", "aidw_r_exp", "aidw_dtype_of", "aidw_knn_robs", "aidw_alpha", "aidw_interpolate",
-    "aidw_run_host", "aidw_check", "aidw_launch_count", "aidw_destroy",
+    "aidw_run_host", "aidw_check", "aidw_launch_count", "aidw_destroy", "aidw_run_fixed", "aidw_idw",
 )
 
 
@@ -80,6 +80,8 @@ def lib():
             "aidw_run_host": ([P, P, P, I64, I, P, I, D, D, I, P, P], I),
             "aidw_check": ([P, P], I),
             "aidw_launch_count": ([P], I64),
+            "aidw_run_fixed": ([P, P, P, I64, I, P, D, D, I, P, P, P, P], I),
+            "aidw_idw": ([P, P, P, I64, D, P, P], I),
             "aidw_destroy": ([P], I),
         }
         for name, (args, res) in sig.items():
@@ -143,6 +145,15 @@ def aidw_run_host(h, qx_host, qy_host, k, levels, rbounds, r_min, r_max, muform,
     _err(h, lib().aidw_run_host(h, _ptr(qx_host), _ptr(qy_host), qx_host.numel(), int(k), _levels(levels),
                                 int(rbounds), float(r_min), float(r_max), int(muform), _ptr(z_host),
                                 _stream(stream)))
+
+
+def aidw_run_fixed(h, qx, qy, k, levels, r_min, r_max, muform, z, r_obs=None, alpha=None, stream=None):
+    _err(h, lib().aidw_run_fixed(h, _ptr(qx), _ptr(qy), qx.numel(), int(k), _levels(levels), float(r_min),
+                                 float(r_max), int(muform), _ptr(z), _ptr(r_obs), _ptr(alpha), _stream(stream)))
+
+
+def aidw_idw(h, qx, qy, alpha, z, stream=None):
+    _err(h, lib().aidw_idw(h, _ptr(qx), _ptr(qy), qx.numel(), float(alpha), _ptr(z), _stream(stream)))
 
 
 def aidw_check(h, stream=None):
@@ -239,6 +250,26 @@ class AIDW:
         z = self.interpolate(qx, qy, a, d1sq, stream)
         if trace:
             return z, dict(r_obs=r_obs, d1sq=d1sq, minmax=mm, alpha=a)
+        return z
+
+    def run_fixed(self, qx, qy, k=10, levels=LEVELS_DEFAULT, r_min=0.0, r_max=2.0, muform=NORMALIZED,
+                  stream=None, trace=False):
+        """N1: FIXED-bounds AIDW in one fused launch (aidw_run_fixed)."""
+        qx, qy = self._q(qx), self._q(qy)
+        n = qx.numel()
+        z = self._empty(n)
+        r_obs = self._empty(n) if trace else None
+        a = self._empty(n) if trace else None
+        aidw_run_fixed(self.h, qx, qy, k, levels, r_min, r_max, muform, z, r_obs, a, stream)
+        if trace:
+            return z, dict(r_obs=r_obs, alpha=a)
+        return z
+
+    def idw(self, qx, qy, alpha=2.0, stream=None):
+        """N2: standard IDW with a constant power (aidw_idw)."""
+        qx, qy = self._q(qx), self._q(qy)
+        z = self._empty(qx.numel())
+        aidw_idw(self.h, qx, qy, alpha, z, stream)
         return z
 
     def run_host(self, qx_host, qy_host, k=10, levels=LEVELS_DEFAULT, rbounds=GLOBAL, r_min=0.0, r_max=2.0,

@@ -9,8 +9,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libaidw.so")
-SOURCES = ["aidw_api.cu", "knn_robs.cu", "interpolate.cu", "alpha_prep.cu"]
-HEADERS = ["aidw_internal.h", "device.cuh", "packed.cuh"]
+SOURCES = ["aidw_api.cu", "knn_robs.cu", "interpolate.cu", "alpha_prep.cu", "fused.cu"]
+HEADERS = ["aidw_internal.h", "device.cuh", "packed.cuh", "passes.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -312,10 +312,10 @@ aidw_status aidw_interpolate(aidw_t h, const void *qx, const void *qy, int64_t n
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (!d1sq) {  // nearest squared distance via the k = 1 kNN pass
         const size_t ts = tsize(h->dt);
-        aidw_status s = ensure_work(h, 2 * (size_t)nq * ts);
+        aidw_status s = ensure_work(h, 2 * (((size_t)nq * ts + 255) / 256 * 256));
         if (s != AIDW_OK) return s;
         void *robs = h->work;
-        void *d1 = static_cast<char *>(h->work) + (size_t)nq * ts;
+        void *d1 = static_cast<char *>(h->work) + ((size_t)nq * ts + 255) / 256 * 256;
         s = launched(h,
                      aidw::launch_knn((int)h->dt, 1, h->data, h->ndp, qx, qy, nq, robs, d1, nullptr, nullptr,
                                       h->sc, &h->filt, st),
@@ -323,7 +323,69 @@ aidw_status aidw_interpolate(aidw_t h, const void *qx, const void *qy, int64_t n
         if (s != AIDW_OK) return s;
         d1sq = d1;
     }
-    return launched(h, aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, alpha, d1sq, z_out, st),
+    return launched(h,
+                    aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, alpha, 0.0, d1sq, z_out, st),
+                    "interpolate kernel");
+}
+
+aidw_status aidw_run_fixed(aidw_t h, const void *qx, const void *qy, int64_t nq, int k, const double *alpha_lv,
+                           double r_min, double r_max, aidw_muform mf, void *z_out, void *r_obs_out,
+                           void *alpha_out, void *stream)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    if (nq < 0) return fail(h, AIDW_E_INVALID_ARG, "nq < 0");
+    aidw_status s = check_levels(h, alpha_lv);
+    if (s != AIDW_OK) return s;
+    if (!(std::isfinite(r_min) && std::isfinite(r_max)))
+        return fail(h, AIDW_E_INVALID_BOUNDS, "r_min/r_max must be finite");
+    if (!(r_min < r_max)) return fail(h, AIDW_E_INVALID_BOUNDS, "r_min = %g >= r_max = %g", r_min, r_max);
+    if (mf != AIDW_MU_NORMALIZED && mf != AIDW_MU_PRINTED) return fail(h, AIDW_E_INVALID_ARG, "bad muform");
+    if (k < 1) return fail(h, AIDW_E_INVALID_ARG, "k = %d must be >= 1", k);
+    if (k > AIDW_KMAX) return fail(h, AIDW_E_UNSUPPORTED, "k = %d > AIDW_KMAX = %d", k, AIDW_KMAX);
+    if (h->nd < k) return fail(h, AIDW_E_INSUFFICIENT_DATA, "nd = %lld < k = %d", (long long)h->nd, k);
+    if (nq == 0) return AIDW_OK;
+    if (!qx || !qy || !z_out) return fail(h, AIDW_E_INVALID_ARG, "qx/qy/z_out is NULL");
+    CK(h, cudaSetDevice(h->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (h->dt == AIDW_F32 && h->filt.arrays)
+        return launched(h,
+                        aidw::launch_fused_fixed(h->data, h->ndp, h->nd, &h->filt, qx, qy, nq, k, h->r_exp, alpha_lv,
+                                                 r_min, r_max, (int)mf, z_out, r_obs_out, alpha_out, h->sc, st),
+                        "fused kernel");
+    // fp64 (or no filter): the three stage kernels on handle scratch
+    const size_t ts = tsize(h->dt);
+    const size_t nb = ((size_t)nq * ts + 255) / 256 * 256;
+    if ((s = ensure_work(h, 3 * nb)) != AIDW_OK) return s;
+    char *w = static_cast<char *>(h->work);
+    void *robs = r_obs_out ? r_obs_out : w, *d1 = w + nb, *al = alpha_out ? alpha_out : w + 2 * nb;
+    if ((s = aidw_knn_robs(h, qx, qy, nq, k, robs, d1, nullptr, nullptr, stream)) != AIDW_OK) return s;
+    if ((s = aidw_alpha(h, robs, nq, alpha_lv, AIDW_RB_FIXED, r_min, r_max, nullptr, mf, al, stream)) != AIDW_OK)
+        return s;
+    return aidw_interpolate(h, qx, qy, nq, al, d1, z_out, stream);
+}
+
+aidw_status aidw_idw(aidw_t h, const void *qx, const void *qy, int64_t nq, double alpha, void *z_out, void *stream)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    if (nq < 0) return fail(h, AIDW_E_INVALID_ARG, "nq < 0");
+    if (!(std::isfinite(alpha) && alpha > 0.0)) return fail(h, AIDW_E_INVALID_ARG, "alpha = %g must be > 0", alpha);
+    if (nq == 0) return AIDW_OK;
+    if (!qx || !qy || !z_out) return fail(h, AIDW_E_INVALID_ARG, "qx/qy/z_out is NULL");
+    CK(h, cudaSetDevice(h->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t ts = tsize(h->dt);
+    const size_t nb = ((size_t)nq * ts + 255) / 256 * 256;
+    aidw_status s = ensure_work(h, 2 * nb);
+    if (s != AIDW_OK) return s;
+    char *w = static_cast<char *>(h->work);
+    s = launched(h,
+                 aidw::launch_knn((int)h->dt, 1, h->data, h->ndp, qx, qy, nq, w, w + nb, nullptr, nullptr, h->sc,
+                                  &h->filt, st),
+                 "nearest kernel");
+    if (s != AIDW_OK) return s;
+    return launched(h,
+                    aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, nullptr, alpha, w + nb,
+                                        z_out, st),
                     "interpolate kernel");
 }
 

@@ -54,8 +54,13 @@ int launch_alpha(int dtype, const void *r_obs, int64_t nq, double r_exp, const d
                  int rb, double rmin, double rmax, const void *minmax, int mf, void *alpha,
                  cudaStream_t st);
 
+int launch_fused_fixed(const void *data, int64_t ndp, int64_t nd, const FilterData *filt, const void *qx,
+                       const void *qy, int64_t nq, int k, double r_exp, const double *lv, double rmin,
+                       double rmax, int mf, void *z, void *r_obs, void *alpha, Scratch *sc, cudaStream_t st);
+
+// alpha == nullptr -> every query uses alpha_const (standard IDW, Eq. 1 with a constant power)
 int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const void *qx,
-                  const void *qy, int64_t nq, const void *alpha, const void *d1sq, void *z,
+                  const void *qy, int64_t nq, const void *alpha, double alpha_const, const void *d1sq, void *z,
                   cudaStream_t st);
 
 }  // namespace aidw

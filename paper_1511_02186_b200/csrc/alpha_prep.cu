@@ -1,6 +1,5 @@
 // alpha_prep.cu -- S0 (repack + bounding box) and S4 (R, mu_R, alpha) kernels.
-#include "aidw_internal.h"
-#include "device.cuh"
+#include "passes.cuh"
 
 namespace aidw {
 
@@ -133,12 +132,7 @@ int launch_center(const void *data, int64_t ndp, int64_t nd, float c_x, float c_
 }
 
 // ------------------------------------------------------------------ S4: alpha
-struct Levels {
-    double a[5];
-};
-
-// Eq. 4, Eq. 5, Eq. 6,
-// all in fp64 (R24); intervals resolve first-match in printed order.
+// Eq. 4-6 per query in fp64 (passes.cuh alpha_eq); GLOBAL bounds read on the device.
 template <typename T>
 __global__ void alpha_kernel(const T *__restrict__ robs, int64_t nq, double r_exp, Levels lv, int rb,
                              double rmin, double rmax, const T *__restrict__ mm, int mf,
@@ -149,31 +143,8 @@ __global__ void alpha_kernel(const T *__restrict__ robs, int64_t nq, double r_ex
         rmax = (double)mm[1] / r_exp;
     }
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const double R = (double)robs[i] / r_exp;
-        double mu;
-        if (R <= rmin)
-            mu = 0.0;
-        else if (R <= rmax)
-            mu = (mf == 0) ? 0.5 - 0.5 * cospi((R - rmin) / (rmax - rmin))
-                           : 0.5 - 0.5 * cos(3.141592653589793 / rmax * (R - rmin));
-        else
-            mu = 1.0;
-        double al;
-        if (mu <= 0.1)
-            al = lv.a[0];
-        else if (mu <= 0.3)
-            al = lv.a[0] * (1.0 - 5.0 * (mu - 0.1)) + 5.0 * lv.a[1] * (mu - 0.1);
-        else if (mu <= 0.5)
-            al = 5.0 * lv.a[2] * (mu - 0.3) + lv.a[1] * (1.0 - 5.0 * (mu - 0.3));
-        else if (mu <= 0.7)
-            al = lv.a[2] * (1.0 - 5.0 * (mu - 0.5)) + 5.0 * lv.a[3] * (mu - 0.5);
-        else if (mu <= 0.9)
-            al = 5.0 * lv.a[4] * (mu - 0.7) + lv.a[3] * (1.0 - 5.0 * (mu - 0.7));
-        else
-            al = lv.a[4];
-        alpha[i] = (T)al;
-    }
+         i += (int64_t)gridDim.x * blockDim.x)
+        alpha[i] = (T)alpha_eq((double)robs[i], r_exp, rmin, rmax, mf, lv);
 }
 
 int launch_alpha(int dtype, const void *r_obs, int64_t nq, double r_exp, const double *lvp, int rb,

@@ -1,0 +1,180 @@
+// fused.cu -- N1: FIXED-bounds AIDW in ONE kernel, the paper's
+// per-thread structure (kNN -> r_obs -> R -> mu -> alpha -> weighting pass, PAPER.md
+// :407-438, Fig. 3) rebuilt on the same sm_100a tile passes as the 3-kernel path.
+//
+// With caller-given R_min / R_max (Eq. 5's "in general 0.0 and 2.0")
+// no query waits for any other, so there is no phase barrier: every CTA runs its kNN
+// tiles, computes alpha in registers, and streams the data again for Eq. 1.  CTAs of
+// the same SM are then at different phases, so the FMA/ALU-bound kNN pass and the
+// SFU-bound weighting pass share the SM's pipes.  One TMA ring
+// carries both passes: tiles 0..nt-1 are (cx, cy, pp, x, y) kNN tiles, tiles nt..2nt-1
+// are (x, y, z) weighting tiles, so the weighting data is prefetched while the last
+// kNN tiles are being consumed.  Results are identical to the 3-kernel path in FIXED
+// mode (same tile functions, same operation order).
+#include "passes.cuh"
+
+namespace aidw {
+
+struct FusedArgs {
+    const float *px, *py, *pz;  // internal SoA, padded
+    int64_t ndp, nd;
+    FilterArgs f;
+    const float *qx, *qy;
+    int64_t nq;
+    int k;
+    double r_exp;
+    Levels lv;
+    double rmin, rmax;
+    int mf;
+    float *z, *r_obs, *alpha;  // r_obs / alpha nullable
+    Scratch *sc;
+};
+
+template <int K, int Q, int G, unsigned EMU>
+__global__ void __launch_bounds__(kBlock) fused_fixed_kernel(const FusedArgs a)
+{
+    constexpr int TILE = kTileKF, STAGES = kStagesKF;
+    static_assert(TILE == kTileW, "both passes use the same tile (fp32 sums are per kTileW)");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *sm = reinterpret_cast<float *>(smem_raw);  // stage s at sm + s * 5 * TILE
+    Ring<STAGES> ring{reinterpret_cast<uint64_t *>(sm + STAGES * 5 * TILE),
+                      reinterpret_cast<uint64_t *>(sm + STAGES * 5 * TILE) + STAGES};
+    const int nt = (int)(a.ndp / TILE);
+    const int ntot = 2 * nt;
+    if (threadIdx.x == 0) ring.init();
+    __syncthreads();
+
+    auto issue = [&](int gt, int slot) {
+        constexpr uint32_t B = TILE * sizeof(float);
+        float *d = sm + slot * 5 * TILE;
+        if (gt < nt) {
+            const int64_t off = (int64_t)gt * TILE;
+            mbar_arrive_expect_tx(&ring.full[slot], 5u * B);
+            bulk_g2s(d, a.f.cx + off, B, &ring.full[slot]);
+            bulk_g2s(d + TILE, a.f.cy + off, B, &ring.full[slot]);
+            bulk_g2s(d + 2 * TILE, a.f.pp + off, B, &ring.full[slot]);
+            bulk_g2s(d + 3 * TILE, a.px + off, B, &ring.full[slot]);
+            bulk_g2s(d + 4 * TILE, a.py + off, B, &ring.full[slot]);
+        } else {
+            const int64_t off = (int64_t)(gt - nt) * TILE;
+            mbar_arrive_expect_tx(&ring.full[slot], 3u * B);
+            bulk_g2s(d, a.px + off, B, &ring.full[slot]);
+            bulk_g2s(d + TILE, a.py + off, B, &ring.full[slot]);
+            bulk_g2s(d + 2 * TILE, a.pz + off, B, &ring.full[slot]);
+        }
+    };
+    if (threadIdx.x == 0)
+        for (int s = 0; s < STAGES && s < ntot; ++s) issue(s, s);
+
+    const int64_t base = (int64_t)blockIdx.x * (kBlock * Q) + threadIdx.x;
+    float qx[Q], qy[Q];
+    bool valid[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int64_t idx = base + q * kBlock;
+        valid[q] = idx < a.nq;
+        qx[q] = valid[q] ? a.qx[idx] : 0.f;
+        qy[q] = valid[q] ? a.qy[idx] : 0.f;
+        if (valid[q] && !(isfinite(qx[q]) && isfinite(qy[q]))) atomicMin(&a.sc->err_idx, (long long)idx);
+    }
+
+    // ---- pass 1: kNN (S1), r_obs (S2)
+    const int k0 = K - a.k;
+    float d1[Q], al[Q];
+    {
+        KnnF32State<K, Q> st;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) st.init(q, qx[q], qy[q], a.f, k0);
+        for (int t = 0; t < nt; ++t) {
+            ring.wait_full(t);
+            const float *d = sm + ring.slot(t) * 5 * TILE;
+            knn_f32_tile<K, Q, G, TILE>(st, d, d + TILE, d + 2 * TILE, d + 3 * TILE, d + 4 * TILE);
+            ring.release(t, ntot, issue);
+        }
+        // ---- S4 in registers: R, mu, alpha (fp64) with the FIXED bounds
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            float robs;
+            robs_of<float, K>(st.buf[q], k0, a.k, robs, d1[q]);
+            al[q] = (float)alpha_eq((double)robs, a.r_exp, a.rmin, a.rmax, a.mf, a.lv);
+            const int64_t idx = base + q * kBlock;
+            if (valid[q]) {
+                if (a.r_obs) a.r_obs[idx] = robs;
+                if (a.alpha) a.alpha[idx] = al[q];
+            }
+        }
+    }
+
+    // ---- pass 2: weighting (S5)
+    InterpF32State<Q> st2;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) st2.init(q, qx[q], qy[q], al[q], d1[q]);
+    for (int t = nt; t < ntot; ++t) {
+        ring.wait_full(t);
+        const float *d = sm + ring.slot(t) * 5 * TILE;
+        interp_f32_tile<Q, EMU, TILE>(st2, d, d + TILE, d + 2 * TILE);
+        ring.release(t, ntot, issue);
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        if (!valid[q]) continue;
+        double zq = st2.SWZ[q] / st2.SW[q];
+        if (d1[q] == 0.f) zq = coincident_mean<float>(qx[q], qy[q], a.px, a.py, a.pz, a.nd);  // R19
+        a.z[base + q * kBlock] = (float)zq;
+    }
+}
+
+template <int K, int Q = 2, int G = 8, unsigned EMU = 0x5>
+static int launch_fused_t(const FusedArgs &a, cudaStream_t st)
+{
+    const size_t smem = (size_t)5 * kStagesKF * kTileKF * sizeof(float) + 2 * kStagesKF * sizeof(uint64_t);
+    if (cudaFuncSetAttribute(fused_fixed_kernel<K, Q, G, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(fused_fixed_kernel<K, Q, G, EMU>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             100) != cudaSuccess)
+        return -1;
+    const int64_t per_cta = (int64_t)kBlock * Q;
+    const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
+    fused_fixed_kernel<K, Q, G, EMU><<<grid, kBlock, smem, st>>>(a);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_fused_fixed(const void *data, int64_t ndp, int64_t nd, const FilterData *filt, const void *qx,
+                       const void *qy, int64_t nq, int k, double r_exp, const double *lvp, double rmin,
+                       double rmax, int mf, void *z, void *r_obs, void *alpha, Scratch *sc, cudaStream_t st)
+{
+    const float *p = static_cast<const float *>(data);
+    const float *c = static_cast<const float *>(filt->arrays);
+    FusedArgs a;
+    a.px = p;
+    a.py = p + ndp;
+    a.pz = p + 2 * ndp;
+    a.ndp = ndp;
+    a.nd = nd;
+    a.f = FilterArgs{c, c + ndp, c + 2 * ndp, filt->c_x, filt->c_y, filt->r1};
+    a.qx = (const float *)qx;
+    a.qy = (const float *)qy;
+    a.nq = nq;
+    a.k = k;
+    a.r_exp = r_exp;
+    for (int i = 0; i < 5; ++i) a.lv.a[i] = lvp[i];
+    a.rmin = rmin;
+    a.rmax = rmax;
+    a.mf = mf;
+    a.z = (float *)z;
+    a.r_obs = (float *)r_obs;
+    a.alpha = (float *)alpha;
+    a.sc = sc;
+    if (k <= 1) return launch_fused_t<1>(a, st);
+    if (k <= 2) return launch_fused_t<2>(a, st);
+    if (k <= 4) return launch_fused_t<4>(a, st);
+    if (k <= 8) return launch_fused_t<8>(a, st);
+    if (k <= 10) return launch_fused_t<10>(a, st);
+    if (k <= 12) return launch_fused_t<12>(a, st);
+    if (k <= 15) return launch_fused_t<15>(a, st);
+    if (k <= 16) return launch_fused_t<16>(a, st);
+    if (k <= 24) return launch_fused_t<24>(a, st);
+    return launch_fused_t<32>(a, st);
+}
+
+}  // namespace aidw

@@ -1,0 +1,312 @@
+// passes.cuh -- the two O(nq*nd) passes of the AIDW hot path as per-tile device
+// functions, shared by the stand-alone kernels (knn_robs.cu, interpolate.cu) and the
+// fused FIXED-bounds kernel (fused.cu).  Also the TMA/mbarrier tile ring, the exact
+// kNN epilogue pieces and the Eq. 4-6 map.
+#pragma once
+
+#include "aidw_internal.h"
+#include "device.cuh"
+#include "packed.cuh"
+
+namespace aidw {
+
+// ------------------------------------------------------------------ tile ring
+// STAGES smem slots filled by the TMA engine (one elected producer thread), consumed
+// by all warps.  Tile t lives in slot t % STAGES; full/empty barrier parity (t/S) & 1.
+template <int STAGES>
+struct Ring {
+    uint64_t *full, *empty;
+
+    __device__ __forceinline__ void init()  // thread 0, then __syncthreads by the caller
+    {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kWarps);
+        }
+        fence_mbar_init();
+    }
+    __device__ __forceinline__ int slot(int t) const { return t % STAGES; }
+    __device__ __forceinline__ uint32_t parity(int t) const { return (uint32_t)(t / STAGES) & 1u; }
+    __device__ __forceinline__ void wait_full(int t) { mbar_wait(&full[slot(t)], parity(t)); }
+    // every warp releases the slot; the producer refills it with tile t + STAGES
+    template <class Issue>
+    __device__ __forceinline__ void release(int t, int ntotal, Issue &&issue)
+    {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot(t)]);
+        if (threadIdx.x == 0 && t + STAGES < ntotal) {
+            mbar_wait(&empty[slot(t)], parity(t));
+            issue(t + STAGES, slot(t));
+        }
+    }
+};
+
+// ------------------------------------------------------------------ kNN pieces
+// Sorted insertion of s into ascending b[0..K-1], dropping the largest:
+// b'[i] = min(b[i], max(b[i-1], s)), b'[0] = min(b[0], s).  Equivalent to Step 3's
+// replace-the-kth-then-bubble for s < b[K-1]; a no-op otherwise.
+template <typename T, int K>
+__device__ __forceinline__ void topk_insert(T (&b)[K], T s)
+{
+#pragma unroll
+    for (int i = K - 1; i > 0; --i) b[i] = tmin(b[i], tmax(b[i - 1], s));
+    b[0] = tmin(b[0], s);
+}
+
+// r_obs (Eq. 3: ascending sum of the k distances, then /k) and the nearest s of one
+// query's register list (slots [0, k0) are -inf sentinels).
+template <typename T, int K>
+__device__ __forceinline__ void robs_of(const T (&b)[K], int k0, int k, T &robs, T &d1)
+{
+    T sum = T(0);
+    d1 = b[K - 1];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        if (i >= k0) sum = add_rn(sum, sqrt_rn(b[i]));
+        if (i == k0) d1 = b[i];
+    }
+    robs = div_rn(sum, (T)k);
+}
+
+// ---------------------------------------------------------------------------------
+// fp32 kNN with an exact-safe expanded-form filter.
+//
+// With centred coordinates p' = p - c, q' = q - c (c = bbox centre, fp32), the squared
+// distance is s' = |q'|^2 + t,  t = |p'|^2 - 2 q'.p'.  t is evaluated with two packed
+// FFMA2 per couple of points from per-point |p'|^2 (precomputed once per handle): 2 FMA
+// + a share of a min-tree per pair instead of 4 FP32 + 1 compare.  A pair can only
+// enter the top-k if t <= thr_f, where thr_f is the current k-th canonical distance
+// converted to the t scale with a rigorous rounding margin (thr_of); passing pairs are
+// re-evaluated with the CANONICAL sequence (R16) on the original coordinates and the
+// insertion decision is taken on that exact value, so the selected multiset is bit-for-
+// bit the one of the unfiltered kernel / the oracle's float instantiation.
+//
+// Margin (n1 = |q'x| + |q'y|, R1 >= max_p |p'x| + |p'y|, u = 2^-24):
+//   |t~ - t| <= 4u (n1 + R1)^2         (pp rounding 2u|p'|^2, two FMA roundings u|t|)
+//   canonical s >= D (1 - 4u), D the exact distance^2;  centring moves sqrt(s') by at
+//   most 2u (n1 + R1).  Hence s < thr  =>  t~ < (sqrt(thr)(1+4u) + 4u(n1+R1))^2 - |q'|^2
+//   + 8u(n1+R1)^2; the constants below double every term.
+struct FilterArgs {
+    const float *cx, *cy, *pp;  // centred filter arrays, padded with +inf
+    float c_x, c_y;             // centre
+    float r1;                   // R1 bound
+};
+
+// thr_of: the filter threshold for the canonical k-th distance thr, in fp32 with every
+// rounding error covered: sqrt rounded up, (1 + 2^-20) and 2^-21 slack terms absorb
+// the <= 3 roundings of the remaining fp32 operations.
+//   qq = |q'|^2 (rounded up), m = 8u(n1+R1) (centring), E = 16u(n1+R1)^2 + 6u qq.
+__device__ __forceinline__ float thr_of(float thr, float qq, float m, float E)
+{
+    if (!(thr < pos_inf<float>())) return pos_inf<float>();
+    const float r = __fmaf_ru(__fsqrt_ru(thr), 1.0f + 0x1p-20f, m);
+    const float r2 = __fmul_ru(r, r);
+    const float v = __fadd_ru(__fadd_ru(r2, -qq), E);
+    return __fmaf_ru(0x1p-21f, r2 + qq + E, v);
+}
+
+// Per-thread state of the filtered kNN for Q queries.
+template <int K, int Q>
+struct KnnF32State {
+    float qx[Q], qy[Q], thr[Q], qqf[Q], mf[Q], Ef[Q], A[Q], B[Q];
+    float buf[Q][K];
+
+    __device__ __forceinline__ void init(int q, float x, float y, const FilterArgs &f, int k0)
+    {
+        qx[q] = x;
+        qy[q] = y;
+        const float qcx = __fsub_rn(x, f.c_x), qcy = __fsub_rn(y, f.c_y);
+        A[q] = -2.0f * qcx;
+        B[q] = -2.0f * qcy;
+        thr[q] = pos_inf<float>();
+        const double u = 0x1p-24;
+        const double qq = (double)qcx * (double)qcx + (double)qcy * (double)qcy;
+        const double n1r = fabs((double)qcx) + fabs((double)qcy) + (double)f.r1;
+        qqf[q] = __double2float_ru(qq);
+        mf[q] = __double2float_ru(8.0 * u * n1r);
+        Ef[q] = __double2float_ru(16.0 * u * n1r * n1r + 6.0 * u * qq);
+#pragma unroll
+        for (int i = 0; i < K; ++i) buf[q][i] = (i < k0) ? -pos_inf<float>() : pos_inf<float>();
+    }
+};
+
+// One smem tile of TILE points: filter values in groups of G points per warp vote;
+// the next group's smem loads are issued right after the current group's filter
+// values are formed, so they overlap the vote; a bitmask rare path re-checks only the
+// passing pairs with the canonical distance.
+template <int K, int Q, int G, int TILE>
+__device__ __forceinline__ void knn_f32_tile(KnnF32State<K, Q> &st, const float *__restrict__ tcx,
+                                             const float *__restrict__ tcy, const float *__restrict__ tpp,
+                                             const float *__restrict__ tpx, const float *__restrict__ tpy)
+{
+    static_assert(G % 4 == 0 && G <= 32 && TILE % G == 0, "group size");
+    float cxv[G], cyv[G], ppv[G];
+    auto load = [&](int j) {
+#pragma unroll
+        for (int g = 0; g < G; g += 4) {
+            const float4 CX = *reinterpret_cast<const float4 *>(tcx + j + g);
+            const float4 CY = *reinterpret_cast<const float4 *>(tcy + j + g);
+            const float4 PP = *reinterpret_cast<const float4 *>(tpp + j + g);
+            cxv[g] = CX.x; cxv[g + 1] = CX.y; cxv[g + 2] = CX.z; cxv[g + 3] = CX.w;
+            cyv[g] = CY.x; cyv[g + 1] = CY.y; cyv[g + 2] = CY.z; cyv[g + 3] = CY.w;
+            ppv[g] = PP.x; ppv[g + 1] = PP.y; ppv[g + 2] = PP.z; ppv[g + 3] = PP.w;
+        }
+    };
+    load(0);
+#pragma unroll 1
+    for (int j = 0; j < TILE; j += G) {
+        float tv[Q][G];
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+#pragma unroll
+            for (int h = 0; h < G / 2; ++h) {
+                const f32x2 tt = fma2(splat2(st.B[q]), pack2(cyv[2 * h], cyv[2 * h + 1]),
+                                      fma2(splat2(st.A[q]), pack2(cxv[2 * h], cxv[2 * h + 1]),
+                                           pack2(ppv[2 * h], ppv[2 * h + 1])));
+                tv[q][2 * h] = tt.x;
+                tv[q][2 * h + 1] = tt.y;
+            }
+        load(j + G < TILE ? j + G : j);
+        bool hit = false;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            float m[G];
+#pragma unroll
+            for (int i = 0; i < G; ++i) m[i] = tv[q][i];
+#pragma unroll
+            for (int w = 1; w < G; w *= 2)
+#pragma unroll
+                for (int i = 0; i + w < G; i += 2 * w) m[i] = fminf(m[i], m[i + w]);
+            hit |= m[0] <= st.thr[q];
+        }
+        if (__any_sync(0xffffffffu, hit)) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                unsigned mask = 0;
+#pragma unroll
+                for (int e = 0; e < G; ++e) mask |= (tv[q][e] <= st.thr[q]) ? (1u << e) : 0u;
+                while (__any_sync(0xffffffffu, mask != 0)) {
+                    if (mask) {
+                        const int e = __ffs(mask) - 1;
+                        mask &= mask - 1;
+                        const float s = dist_sq(st.qx[q], st.qy[q], tpx[j + e], tpy[j + e]);
+                        if (s < st.buf[q][K - 1]) {
+                            topk_insert<float, K>(st.buf[q], s);
+                            st.thr[q] = thr_of(st.buf[q][K - 1], st.qqf[q], st.mf[q], st.Ef[q]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ Eq. 4-6
+struct Levels {
+    double a[5];
+};
+
+// R = r_obs / r_exp (Eq. 4); mu (Eq. 5, first match
+// in printed order, R8/R9/R10); alpha (Eq. 6, R12).  fp64 (R24).
+__device__ __forceinline__ double alpha_eq(double robs, double r_exp, double rmin, double rmax, int mf,
+                                           const Levels &lv)
+{
+    const double R = robs / r_exp;
+    double mu;
+    if (R <= rmin)
+        mu = 0.0;
+    else if (R <= rmax)
+        mu = (mf == 0) ? 0.5 - 0.5 * cospi((R - rmin) / (rmax - rmin))
+                       : 0.5 - 0.5 * cos(3.141592653589793 / rmax * (R - rmin));
+    else
+        mu = 1.0;
+    if (mu <= 0.1) return lv.a[0];
+    if (mu <= 0.3) return lv.a[0] * (1.0 - 5.0 * (mu - 0.1)) + 5.0 * lv.a[1] * (mu - 0.1);
+    if (mu <= 0.5) return 5.0 * lv.a[2] * (mu - 0.3) + lv.a[1] * (1.0 - 5.0 * (mu - 0.3));
+    if (mu <= 0.7) return lv.a[2] * (1.0 - 5.0 * (mu - 0.5)) + 5.0 * lv.a[3] * (mu - 0.5);
+    if (mu <= 0.9) return 5.0 * lv.a[4] * (mu - 0.7) + lv.a[3] * (1.0 - 5.0 * (mu - 0.7));
+    return lv.a[4];
+}
+
+// ------------------------------------------------------------------ weighting pass
+// Per-thread state of the packed fp32 weighting pass for Q queries:
+// w = 2^(c log2 s + b), c = -alpha/2, b = (alpha/2) log2(d1^2)  (R20).
+template <int Q>
+struct InterpF32State {
+    f32x2 QX[Q], QY[Q], C[Q], B[Q];
+    double SW[Q], SWZ[Q];
+
+    __device__ __forceinline__ void init(int q, float x, float y, float alpha, float d1sq)
+    {
+        const float c = -0.5f * alpha;
+        const float b = 0.5f * alpha * lg2_approx_noftz(d1sq);
+        QX[q] = splat2(x);
+        QY[q] = splat2(y);
+        C[q] = splat2(c);
+        B[q] = splat2(b);
+        SW[q] = 0.0;
+        SWZ[q] = 0.0;
+    }
+};
+
+// One smem tile of the fp32 weighting pass with packed fp32x2 arithmetic.  Two
+// consecutive data points of one query form a "couple" in one register pair; the fp32
+// tile sums are {even, odd} partial sums folded into fp64 at the end of the tile (R21).
+// The ex2 of couple (q, h) runs on the FMA pipe (exp2_poly2) when bit 2q+h of EMU is
+// set, on the SFU otherwise.
+template <int Q, unsigned EMU, int TILE>
+__device__ __forceinline__ void interp_f32_tile(InterpF32State<Q> &st, const float *__restrict__ tx,
+                                                const float *__restrict__ ty, const float *__restrict__ tz)
+{
+    f32x2 sw[Q], swz[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) sw[q] = swz[q] = make_float2(0.f, 0.f);
+#pragma unroll 2
+    for (int j = 0; j < TILE; j += 4) {
+        const float4 X = *reinterpret_cast<const float4 *>(tx + j);
+        const float4 Y = *reinterpret_cast<const float4 *>(ty + j);
+        const float4 Z = *reinterpret_cast<const float4 *>(tz + j);
+        const f32x2 Xh[2] = {pack2(X.x, X.y), pack2(X.z, X.w)};
+        const f32x2 Yh[2] = {pack2(Y.x, Y.y), pack2(Y.z, Y.w)};
+        const f32x2 Zh[2] = {pack2(Z.x, Z.y), pack2(Z.z, Z.w)};
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const f32x2 dx = sub2(st.QX[q], Xh[h]);
+                const f32x2 dy = sub2(st.QY[q], Yh[h]);
+                const f32x2 s = fma2(dx, dx, mul2(dy, dy));
+                const f32x2 l = pack2(lg2_approx(s.x), lg2_approx(s.y));
+                const f32x2 e = fma2(st.C[q], l, st.B[q]);
+                f32x2 w;
+                if (EMU & (1u << (2 * q + h)))
+                    w = exp2_poly2(e);
+                else
+                    w = pack2(ex2_approx(e.x), ex2_approx(e.y));
+                sw[q] = add2(sw[q], w);
+                swz[q] = fma2(w, Zh[h], swz[q]);
+            }
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        st.SW[q] += (double)sw[q].x + (double)sw[q].y;
+        st.SWZ[q] += (double)swz[q].x + (double)swz[q].y;
+    }
+}
+
+// Exact coincidence (R19): the limit of Eq. 1 is the mean z of the data points at
+// distance 0.  Rare; one extra pass over global memory for the calling lane.
+template <typename T>
+__device__ __forceinline__ double coincident_mean(T qx, T qy, const T *px, const T *py, const T *pz, int64_t nd)
+{
+    double zc = 0.0;
+    long long cnt = 0;
+    for (int64_t i = 0; i < nd; ++i)
+        if (dist_sq(qx, qy, px[i], py[i]) == T(0)) {
+            zc += (double)pz[i];
+            ++cnt;
+        }
+    return zc / (double)cnt;
+}
+
+}  // namespace aidw

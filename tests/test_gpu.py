@@ -293,3 +293,50 @@ def test_launch_count(P):
     n0 = eng.launches
     eng.run(qx, qy, 10)
     assert eng.launches - n0 == 3  # knn_robs, alpha, interpolate
+
+
+# ------------------------------------------------------------------ N1 / N2
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("k", [10, 15, 1])
+def test_run_fixed_fused(P, orc, dtype, k):
+    """N1: one fused launch == the three stage kernels in FIXED mode (bit-identical),
+    and within tolerance of the oracle."""
+    x, y, z, qx, qy = datagen.random_cloud(50 + k, 7001, 1333)
+    eng = P.AIDW(x, y, z, dtype=dtype)
+    n0 = eng.launches
+    zf, tf = eng.run_fixed(qx, qy, k, LV, 0.0, 2.0, trace=True)
+    assert eng.launches - n0 == (1 if dtype == torch.float32 else 3)
+    z3, t3 = eng.run(qx, qy, k, LV, P.FIXED, 0.0, 2.0, trace=True)
+    assert torch.equal(tf["r_obs"], t3["r_obs"]) and torch.equal(tf["alpha"], t3["alpha"])
+    assert torch.equal(zf, z3)
+    Zo = orc.aidw(x, y, z, qx, qy, k, LV, mode="fixed")
+    assert rel_err(zf.cpu().numpy(), Zo).max() <= TOL[dtype]
+    # a different FIXED window and the printed mu form
+    zf2 = eng.run_fixed(qx, qy, k, LV, 1.0, 3.5, P.PRINTED)
+    Zo2 = orc.aidw(x, y, z, qx, qy, k, LV, mode="fixed", r_min=1.0, r_max=3.5, form=orc.PRINTED)
+    assert rel_err(zf2.cpu().numpy(), Zo2).max() <= TOL[dtype]
+
+
+def test_run_fixed_coincident_and_errors(P, orc):
+    x, y, z, qx, qy = datagen.random_cloud(77, 2000, 50)
+    qx = np.concatenate([qx, x[:7]])
+    qy = np.concatenate([qy, y[:7]])
+    eng = P.AIDW(x, y, z)
+    zf = eng.run_fixed(qx, qy, 10).cpu().numpy()
+    assert np.array_equal(zf[50:], z[:7].astype(np.float32))
+    with pytest.raises(P.AidwError, match="BOUNDS"):
+        eng.run_fixed(qx, qy, 10, LV, 2.0, 1.0)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("alpha", [1.0, 2.0, 2.7])
+def test_idw(P, orc, dtype, alpha):
+    """N2: standard IDW (constant power) against the oracle's Eq. 1."""
+    x, y, z, qx, qy = datagen.random_cloud(60, 9000, 777)
+    eng = P.AIDW(x, y, z, dtype=dtype)
+    Zg = eng.idw(qx, qy, alpha).cpu().numpy()
+    Zo = orc.idw(x, y, z, qx, qy, alpha)
+    assert rel_err(Zg, Zo).max() <= TOL[dtype]
+    # AIDW with constant levels == IDW on the GPU too (same kernel)
+    Za = eng.run(qx, qy, 10, [alpha] * 5).cpu().numpy()
+    assert rel_err(Za, Zo).max() <= TOL[dtype]
