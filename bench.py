@@ -184,11 +184,13 @@ def run_reference(args):
     return 0
 
 
-def workload_name(n):
+def workload_name(n, nq=NQ_PER_GPU, mode="global"):
+    rb = "GLOBAL R bounds" if mode == "global" else "FIXED R bounds (0, 2), fused kernel"
     if n == 1:
-        return "C4: 1,024,000 data x 1,024,000 queries, k=10, fp32, uniform, GLOBAL R bounds"
-    return (f"C4 weak-scaled: 1,024,000 data x {n}x1,024,000 queries ({NQ_PER_GPU} per GPU), k=10, fp32, "
-            f"uniform, GLOBAL R bounds allreduced over {n} GPUs")
+        tag = "C4" if nq == NQ_PER_GPU else "C4-shaped"
+        return f"{tag}: 1,024,000 data x {nq:,} queries, k=10, fp32, uniform, {rb}"
+    return (f"C4 weak-scaled: 1,024,000 data x {n}x{nq:,} queries ({nq} per GPU), k=10, fp32, "
+            f"uniform, {rb}" + (f" allreduced over {n} GPUs" if mode == "global" else ""))
 
 
 def main():
@@ -342,8 +344,9 @@ def main():
             e2e_ms = float(t.item())
         e2e = {"value": nq * world / (e2e_ms / 1e3), "unit": "points/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": 2 * 4 * nq * world, "d2h_bytes_per_step": 4 * nq * world,
-               "api": "aidw_run_host (C ABI, pinned host buffers)" if group is None else
-                      "AIDW.run + torch H2D/D2H (pinned), NCCL allreduce"}
+               "api": ("aidw_run_fixed + torch H2D/D2H (pinned)" if args.mode == "fixed" else
+                       "aidw_run_host (C ABI, pinned host buffers)" if group is None else
+                       "AIDW.run + torch H2D/D2H (pinned), allreduce")}
 
     if rank != 0:
         dist.destroy_process_group()
@@ -398,7 +401,7 @@ def main():
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": workload_name(world), "nd": ND, "nq_per_gpu": nq, "nq_total": nq * world,
+        "config": {"workload": workload_name(world, nq, args.mode), "nd": ND, "nq_per_gpu": nq, "nq_total": nq * world,
                    "k": K_NN, "alpha_levels": list(lv),
                    "rbounds": "global" if args.mode == "global" else "fixed (0, 2), fused single kernel",
                    "mu": "normalized",
