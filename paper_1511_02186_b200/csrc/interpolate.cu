@@ -219,7 +219,11 @@ static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st)
     case 5: return launch_interp_f32x2<2, 0xF>(a, st);       // packed, all-FMA-pipe ex2
     case 9: return launch_interp_f32x2<4, 0x15>(a, st);      // Q=4, 3 of 8 couples emulated
     case 11: return launch_interp_f32x2<2, 0x1>(a, st);      // Q=2, 1 of 4
-    default: return launch_interp_f32x2<2, 0x5>(a, st);      // Q=2, 2 of 4 (best measured, r01)
+    case 12: return launch_interp_f32x2<2, 0x10005>(a, st);  // Q=2, 3 of 8 (groups 2/4 + 1/4)
+    case 13: return launch_interp_f32x2<2, 0x70005>(a, st);  // Q=2, 5 of 8
+    case 14: return launch_interp_f32x2<2, 0x20001>(a, st);  // Q=2, 2 of 8, spread
+    case 3: return launch_interp_f32x2<2, 0x5>(a, st);       // Q=2, 2 of 4
+    default: return launch_interp_f32x2<2, 0x10005>(a, st);  // Q=2, 3 of 8 (best measured, r01)
     }
 }
 

@@ -254,38 +254,54 @@ struct InterpF32State {
 // tile sums are {even, odd} partial sums folded into fp64 at the end of the tile (R21).
 // The ex2 of couple (q, h) runs on the FMA pipe (exp2_poly2) when bit 2q+h of EMU is
 // set, on the SFU otherwise.
+template <int Q, unsigned EMU>
+__device__ __forceinline__ void interp_f32_group(InterpF32State<Q> &st, f32x2 (&sw)[Q], f32x2 (&swz)[Q],
+                                                 const float *__restrict__ tx, const float *__restrict__ ty,
+                                                 const float *__restrict__ tz)
+{
+    const float4 X = *reinterpret_cast<const float4 *>(tx);
+    const float4 Y = *reinterpret_cast<const float4 *>(ty);
+    const float4 Z = *reinterpret_cast<const float4 *>(tz);
+    const f32x2 Xh[2] = {pack2(X.x, X.y), pack2(X.z, X.w)};
+    const f32x2 Yh[2] = {pack2(Y.x, Y.y), pack2(Y.z, Y.w)};
+    const f32x2 Zh[2] = {pack2(Z.x, Z.y), pack2(Z.z, Z.w)};
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const f32x2 dx = sub2(st.QX[q], Xh[h]);
+            const f32x2 dy = sub2(st.QY[q], Yh[h]);
+            const f32x2 s = fma2(dx, dx, mul2(dy, dy));
+            const f32x2 l = pack2(lg2_approx(s.x), lg2_approx(s.y));
+            const f32x2 e = fma2(st.C[q], l, st.B[q]);
+            f32x2 w;
+            if (EMU & (1u << (2 * q + h)))
+                w = exp2_poly2(e);
+            else
+                w = pack2(ex2_approx(e.x), ex2_approx(e.y));
+            sw[q] = add2(sw[q], w);
+            swz[q] = fma2(w, Zh[h], swz[q]);
+        }
+}
+
+// One smem tile of the fp32 weighting pass with packed fp32x2 arithmetic.  Two
+// consecutive data points of one query form a "couple" in one register pair; the fp32
+// tile sums are {even, odd} partial sums folded into fp64 at the end of the tile (R21).
+// Groups of 4 points alternate between two offload patterns: the ex2 of couple (q, h)
+// of an even (odd) group runs on the FMA pipe (exp2_poly2) when bit 2q+h of EMU
+// (EMU >> 16) is set, on the SFU otherwise.
 template <int Q, unsigned EMU, int TILE>
 __device__ __forceinline__ void interp_f32_tile(InterpF32State<Q> &st, const float *__restrict__ tx,
                                                 const float *__restrict__ ty, const float *__restrict__ tz)
 {
+    constexpr unsigned EMU_A = EMU & 0xFFFFu, EMU_B = (EMU >> 16) ? (EMU >> 16) : (EMU & 0xFFFFu);
     f32x2 sw[Q], swz[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) sw[q] = swz[q] = make_float2(0.f, 0.f);
-#pragma unroll 2
-    for (int j = 0; j < TILE; j += 4) {
-        const float4 X = *reinterpret_cast<const float4 *>(tx + j);
-        const float4 Y = *reinterpret_cast<const float4 *>(ty + j);
-        const float4 Z = *reinterpret_cast<const float4 *>(tz + j);
-        const f32x2 Xh[2] = {pack2(X.x, X.y), pack2(X.z, X.w)};
-        const f32x2 Yh[2] = {pack2(Y.x, Y.y), pack2(Y.z, Y.w)};
-        const f32x2 Zh[2] = {pack2(Z.x, Z.y), pack2(Z.z, Z.w)};
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int q = 0; q < Q; ++q) {
-                const f32x2 dx = sub2(st.QX[q], Xh[h]);
-                const f32x2 dy = sub2(st.QY[q], Yh[h]);
-                const f32x2 s = fma2(dx, dx, mul2(dy, dy));
-                const f32x2 l = pack2(lg2_approx(s.x), lg2_approx(s.y));
-                const f32x2 e = fma2(st.C[q], l, st.B[q]);
-                f32x2 w;
-                if (EMU & (1u << (2 * q + h)))
-                    w = exp2_poly2(e);
-                else
-                    w = pack2(ex2_approx(e.x), ex2_approx(e.y));
-                sw[q] = add2(sw[q], w);
-                swz[q] = fma2(w, Zh[h], swz[q]);
-            }
+#pragma unroll 1
+    for (int j = 0; j < TILE; j += 8) {
+        interp_f32_group<Q, EMU_A>(st, sw, swz, tx + j, ty + j, tz + j);
+        interp_f32_group<Q, EMU_B>(st, sw, swz, tx + j + 4, ty + j + 4, tz + j + 4);
     }
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
