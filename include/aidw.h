@@ -189,6 +189,23 @@ AIDW_API aidw_status aidw_idw(aidw_t h, const void *qx, const void *qy, int64_t 
                               void *z_out, void *stream);
 
 /*
+ * aidw_paper_baseline -- N3 (Table-1-shaped ablation): the paper's OWN
+ * kernel designs recompiled for sm_100a, as the prior-art baseline the product kernels
+ * are measured against (NOT the product path):
+ *   variant 0 = naive (§3.2.1: registers + global memory only),
+ *   variant 1 = tiled (§3.2.2: shared-memory tile = block size).
+ * One thread per query: kNN buffer pass (Fig. 1), r_obs, R, mu, alpha in the thread with
+ * FIXED bounds [r_min, r_max], then Eq. 1 with pow() and REAL accumulators.
+ *   dt, lay : T and the data layout: AIDW_SOA (x[nd], y[nd], z[nd]) or AIDW_AOAS
+ *   data    : device, in layout `lay`;  qx, qy : device T[nq];  z_out : device T[nq]
+ *   area    : study area A > 0 (Eq. 2);  k : 1..AIDW_KMAX
+ */
+AIDW_API aidw_status aidw_paper_baseline(int variant, aidw_dtype dt, aidw_layout lay, const void *data,
+                                         int64_t nd, const void *qx, const void *qy, int64_t nq, int k,
+                                         const double *alpha_lv, double area, double r_min, double r_max,
+                                         void *z_out, void *stream);
+
+/*
  * aidw_run_host -- the whole single-GPU path from HOST buffers: H2D of the
  * queries, knn_robs, (GLOBAL: local bounds = the job's bounds), alpha,
  * interpolate, D2H of Z; synchronises `stream` and reports deferred errors.

@@ -44,6 +44,7 @@ EXPORTS = (
     "aidw_abi_version", "aidw_status_string", "aidw_last_error", "aidw_create", "aidw_nd",
     "aidw_area", "aidw_r_exp", "aidw_dtype_of", "aidw_knn_robs", "aidw_alpha", "aidw_interpolate",
     "aidw_run_host", "aidw_check", "aidw_launch_count", "aidw_destroy", "aidw_run_fixed", "aidw_idw",
+    "aidw_paper_baseline",
 )
 
 
@@ -82,6 +83,7 @@ def lib():
             "aidw_launch_count": ([P], I64),
             "aidw_run_fixed": ([P, P, P, I64, I, P, D, D, I, P, P, P, P], I),
             "aidw_idw": ([P, P, P, I64, D, P, P], I),
+            "aidw_paper_baseline": ([I, I, I, P, I64, P, P, I64, I, P, D, D, D, P, P], I),
             "aidw_destroy": ([P], I),
         }
         for name, (args, res) in sig.items():
@@ -154,6 +156,14 @@ def aidw_run_fixed(h, qx, qy, k, levels, r_min, r_max, muform, z, r_obs=None, al
 
 def aidw_idw(h, qx, qy, alpha, z, stream=None):
     _err(h, lib().aidw_idw(h, _ptr(qx), _ptr(qy), qx.numel(), float(alpha), _ptr(z), _stream(stream)))
+
+
+def aidw_paper_baseline(variant, data, nd, qx, qy, k, levels, area, r_min, r_max, z, layout=SOA, stream=None):
+    """N3 ablation: the paper's naive (0) / tiled (1) kernel designs on sm_100a."""
+    dt = F32 if data.dtype == torch.float32 else F64
+    _err(None, lib().aidw_paper_baseline(int(variant), dt, int(layout), _ptr(data), int(nd), _ptr(qx), _ptr(qy),
+                                         qx.numel(), int(k), _levels(levels), float(area), float(r_min),
+                                         float(r_max), _ptr(z), _stream(stream)))
 
 
 def aidw_check(h, stream=None):

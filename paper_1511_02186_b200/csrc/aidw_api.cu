@@ -389,6 +389,27 @@ aidw_status aidw_idw(aidw_t h, const void *qx, const void *qy, int64_t nq, doubl
                     "interpolate kernel");
 }
 
+aidw_status aidw_paper_baseline(int variant, aidw_dtype dt, aidw_layout lay, const void *data, int64_t nd,
+                                const void *qx, const void *qy, int64_t nq, int k, const double *alpha_lv,
+                                double area, double r_min, double r_max, void *z_out, void *stream)
+{
+    if (variant != 0 && variant != 1) return fail(nullptr, AIDW_E_INVALID_ARG, "variant must be 0 or 1");
+    if (dt != AIDW_F32 && dt != AIDW_F64) return fail(nullptr, AIDW_E_UNSUPPORTED, "unknown dtype");
+    if (lay != AIDW_SOA && lay != AIDW_AOAS) return fail(nullptr, AIDW_E_UNSUPPORTED, "layout must be SOA or AOAS");
+    if (!data || !qx || !qy || !z_out || !alpha_lv) return fail(nullptr, AIDW_E_INVALID_ARG, "NULL argument");
+    if (nd < 1 || nq < 0) return fail(nullptr, AIDW_E_INVALID_ARG, "bad sizes");
+    if (!(area > 0.0) || std::isinf(area)) return fail(nullptr, AIDW_E_INVALID_AREA, "area must be > 0");
+    if (k < 1 || k > AIDW_KMAX) return fail(nullptr, AIDW_E_UNSUPPORTED, "k out of range");
+    if (nd < k) return fail(nullptr, AIDW_E_INSUFFICIENT_DATA, "nd < k");
+    if (!(r_min < r_max)) return fail(nullptr, AIDW_E_INVALID_BOUNDS, "r_min >= r_max");
+    if (nq == 0) return AIDW_OK;
+    const double r_exp = 1.0 / (2.0 * std::sqrt((double)nd / area));
+    if (aidw::launch_paper(variant, (int)dt, (int)lay, data, nd, qx, qy, nq, k, r_exp, alpha_lv, r_min, r_max, z_out,
+                           static_cast<cudaStream_t>(stream)) < 0)
+        return cuda_fail(nullptr, cudaGetLastError(), "paper baseline kernel");
+    return AIDW_OK;
+}
+
 aidw_status aidw_check(aidw_t h, void *stream)
 {
     if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");

@@ -58,6 +58,10 @@ int launch_fused_fixed(const void *data, int64_t ndp, int64_t nd, const FilterDa
                        const void *qy, int64_t nq, int k, double r_exp, const double *lv, double rmin,
                        double rmax, int mf, void *z, void *r_obs, void *alpha, Scratch *sc, cudaStream_t st);
 
+int launch_paper(int variant, int dtype, int layout, const void *data, int64_t nd, const void *qx, const void *qy,
+                 int64_t nq, int k, double r_exp, const double *lv, double rmin, double rmax, void *z,
+                 cudaStream_t st);
+
 // alpha == nullptr -> every query uses alpha_const (standard IDW, Eq. 1 with a constant power)
 int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const void *qx,
                   const void *qy, int64_t nq, const void *alpha, double alpha_const, const void *d1sq, void *z,

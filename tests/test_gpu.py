@@ -340,3 +340,21 @@ def test_idw(P, orc, dtype, alpha):
     # AIDW with constant levels == IDW on the GPU too (same kernel)
     Za = eng.run(qx, qy, 10, [alpha] * 5).cpu().numpy()
     assert rel_err(Za, Zo).max() <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("variant", [0, 1])
+def test_paper_baseline_kernels(P, orc, dtype, variant):
+    """N3 ablation baselines (the paper's naive / tiled designs) compute the same AIDW
+    (FIXED bounds); fp32 with the paper's REAL accumulators is looser than the product."""
+    x, y, z, qx, qy = datagen.random_cloud(70 + variant, 5000, 700)
+    dev = torch.device("cuda")
+    t = lambda v: torch.as_tensor(v, dtype=dtype, device=dev)
+    area = orc.bbox_area(x, y)
+    Zo = orc.aidw(x, y, z, qx, qy, 10, LV, mode="fixed")
+    for lay, buf in ((P.SOA, np.concatenate([x, y, z])),
+                     (P.AOAS, np.stack([x, y, z, np.zeros_like(x)], 1).reshape(-1))):
+        zo = torch.empty(len(qx), dtype=dtype, device=dev)
+        P.aidw_paper_baseline(variant, t(buf), len(x), t(qx), t(qy), 10, LV, area, 0.0, 2.0, zo, lay)
+        torch.cuda.synchronize()
+        assert rel_err(zo.cpu().numpy(), Zo).max() <= (1e-3 if dtype == torch.float32 else 1e-10)
