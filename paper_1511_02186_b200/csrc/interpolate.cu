@@ -213,17 +213,17 @@ static int interp_variant()
 
 static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st)
 {
+    // EMU: bit 2g+h = couple h of 4-point group g (of 16) on the FMA pipe
     switch (interp_variant()) {
-    case 1: return launch_interp_t<float, 2>(a, st);         // scalar, all-SFU
-    case 2: return launch_interp_f32x2<2, 0x0>(a, st);       // packed, all-SFU
-    case 5: return launch_interp_f32x2<2, 0xF>(a, st);       // packed, all-FMA-pipe ex2
-    case 9: return launch_interp_f32x2<4, 0x15>(a, st);      // Q=4, 3 of 8 couples emulated
-    case 11: return launch_interp_f32x2<2, 0x1>(a, st);      // Q=2, 1 of 4
-    case 12: return launch_interp_f32x2<2, 0x10005>(a, st);  // Q=2, 3 of 8 (groups 2/4 + 1/4)
-    case 13: return launch_interp_f32x2<2, 0x70005>(a, st);  // Q=2, 5 of 8
-    case 14: return launch_interp_f32x2<2, 0x20001>(a, st);  // Q=2, 2 of 8, spread
-    case 3: return launch_interp_f32x2<2, 0x5>(a, st);       // Q=2, 2 of 4
-    default: return launch_interp_f32x2<2, 0x10005>(a, st);  // Q=2, 3 of 8 (best measured, r01)
+    case 1: return launch_interp_t<float, 2>(a, st);      // scalar, all-SFU
+    case 2: return launch_interp_f32x2<2, 0x00>(a, st);   // packed, all-SFU
+    case 3: return launch_interp_f32x2<2, 0x55>(a, st);   // 4 of 8 couples on the FMA pipe
+    case 4: return launch_interp_f32x2<2, 0x11>(a, st);   // 2 of 8
+    case 5: return launch_interp_f32x2<2, 0xFF>(a, st);   // all on the FMA pipe
+    case 6: return launch_interp_f32x2<2, 0x59>(a, st);   // 4 of 8, spread h
+    case 7: return launch_interp_f32x2<4, 0x19>(a, st);   // Q=4, 3 of 8
+    case 8: return launch_interp_f32x2<2, 0x5D>(a, st);   // 5 of 8
+    default: return launch_interp_f32x2<2, 0x19>(a, st);  // 3 of 8 (best measured, r01)
     }
 }
 

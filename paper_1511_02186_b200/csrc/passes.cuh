@@ -254,7 +254,7 @@ struct InterpF32State {
 // tile sums are {even, odd} partial sums folded into fp64 at the end of the tile (R21).
 // The ex2 of couple (q, h) runs on the FMA pipe (exp2_poly2) when bit 2q+h of EMU is
 // set, on the SFU otherwise.
-template <int Q, unsigned EMU>
+template <int Q, unsigned HMASK>
 __device__ __forceinline__ void interp_f32_group(InterpF32State<Q> &st, f32x2 (&sw)[Q], f32x2 (&swz)[Q],
                                                  const float *__restrict__ tx, const float *__restrict__ ty,
                                                  const float *__restrict__ tz)
@@ -275,7 +275,7 @@ __device__ __forceinline__ void interp_f32_group(InterpF32State<Q> &st, f32x2 (&
             const f32x2 l = pack2(lg2_approx(s.x), lg2_approx(s.y));
             const f32x2 e = fma2(st.C[q], l, st.B[q]);
             f32x2 w;
-            if (EMU & (1u << (2 * q + h)))
+            if (HMASK & (1u << h))
                 w = exp2_poly2(e);
             else
                 w = pack2(ex2_approx(e.x), ex2_approx(e.y));
@@ -287,21 +287,25 @@ __device__ __forceinline__ void interp_f32_group(InterpF32State<Q> &st, f32x2 (&
 // One smem tile of the fp32 weighting pass with packed fp32x2 arithmetic.  Two
 // consecutive data points of one query form a "couple" in one register pair; the fp32
 // tile sums are {even, odd} partial sums folded into fp64 at the end of the tile (R21).
-// Groups of 4 points alternate between two offload patterns: the ex2 of couple (q, h)
-// of an even (odd) group runs on the FMA pipe (exp2_poly2) when bit 2q+h of EMU
-// (EMU >> 16) is set, on the SFU otherwise.
+// The exp2 of couple h of 4-point group g (g = 0..3 within each 16 points) runs on the
+// FMA pipe (exp2_poly2) when bit 2g+h of EMU is set, on the SFU otherwise (DESIGN.md
+// §4.3).  The choice depends on the data-point index only -- never on which register
+// slot holds the query -- so every query's rounding is independent of its position in
+// the launch (bit-identical results for any sharding).
 template <int Q, unsigned EMU, int TILE>
 __device__ __forceinline__ void interp_f32_tile(InterpF32State<Q> &st, const float *__restrict__ tx,
                                                 const float *__restrict__ ty, const float *__restrict__ tz)
 {
-    constexpr unsigned EMU_A = EMU & 0xFFFFu, EMU_B = (EMU >> 16) ? (EMU >> 16) : (EMU & 0xFFFFu);
+    static_assert(TILE % 16 == 0, "tile");
     f32x2 sw[Q], swz[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) sw[q] = swz[q] = make_float2(0.f, 0.f);
 #pragma unroll 1
-    for (int j = 0; j < TILE; j += 8) {
-        interp_f32_group<Q, EMU_A>(st, sw, swz, tx + j, ty + j, tz + j);
-        interp_f32_group<Q, EMU_B>(st, sw, swz, tx + j + 4, ty + j + 4, tz + j + 4);
+    for (int j = 0; j < TILE; j += 16) {
+        interp_f32_group<Q, (EMU >> 0) & 3u>(st, sw, swz, tx + j, ty + j, tz + j);
+        interp_f32_group<Q, (EMU >> 2) & 3u>(st, sw, swz, tx + j + 4, ty + j + 4, tz + j + 4);
+        interp_f32_group<Q, (EMU >> 4) & 3u>(st, sw, swz, tx + j + 8, ty + j + 8, tz + j + 8);
+        interp_f32_group<Q, (EMU >> 6) & 3u>(st, sw, swz, tx + j + 12, ty + j + 12, tz + j + 12);
     }
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
