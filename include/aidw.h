@@ -206,6 +206,44 @@ AIDW_API aidw_status aidw_paper_baseline(int variant, aidw_dtype dt, aidw_layout
                                          void *z_out, void *stream);
 
 /*
+ * N4 -- data-sharded mode: the DATA points are split across handles /
+ * ranks (shard boundaries at multiples of 1024 points keep the fp32 tile sums identical),
+ * every rank evaluates ALL queries against its shard, and the per-shard results are
+ * combined exactly (kNN) or in a fixed rank order (Eq. 1 sums).  Sequence per rank:
+ *   aidw_set_extent(h, nd_total, area)      r_exp of the WHOLE data set (Eq. 2)
+ *   aidw_knn_partial -> allgather lists    -> aidw_knn_merge (r_obs, d1sq, {-min, max})
+ *   aidw_alpha (GLOBAL: the merged bounds already cover all queries)
+ *   aidw_interpolate_partial -> allgather partials -> aidw_finalize (Z)
+ * The merged k-lists, r_obs, d1sq and alpha are bit-identical to a single-device run.
+ */
+/* Set the data-set size and study area used for r_exp (Eq. 2); area > 0, nd_total >= 1. */
+AIDW_API aidw_status aidw_set_extent(aidw_t h, int64_t nd_total, double area);
+
+/* Bounding box of the handle's data: out[4] = {min x, max x, min y, max y} (host). */
+AIDW_API aidw_status aidw_bbox(aidw_t h, double *out);
+
+/* The k smallest SQUARED distances (ascending) of each query to this handle's data:
+ * s_out device T[nq*k].  Same kernel and arithmetic as aidw_knn_robs (R16). */
+AIDW_API aidw_status aidw_knn_partial(aidw_t h, const void *qx, const void *qy, int64_t nq, int k,
+                                      void *s_out, void *stream);
+
+/* Merge P partial lists (device T[P][nq][k], each ascending) into the k smallest, then
+ * r_obs / d1sq / robs_minmax exactly as aidw_knn_robs (any of the three nullable). */
+AIDW_API aidw_status aidw_knn_merge(aidw_t h, const void *lists, int P, int64_t nq, int k, void *r_obs,
+                                    void *d1sq, void *robs_minmax, void *stream);
+
+/* Eq. 1 partial sums over this handle's data: partial_out device double[nq][4] =
+ * {sum w, sum w z, sum z (coincident points), count (coincident points)}; d1sq is the
+ * merged (global) nearest squared distance. */
+AIDW_API aidw_status aidw_interpolate_partial(aidw_t h, const void *qx, const void *qy, int64_t nq,
+                                              const void *alpha, const void *d1sq, double *partial_out,
+                                              void *stream);
+
+/* Z from P partials (device double[P][nq][4]) summed in rank order: z_out device T[nq]. */
+AIDW_API aidw_status aidw_finalize(aidw_t h, const double *partials, int P, int64_t nq, void *z_out,
+                                   void *stream);
+
+/*
  * aidw_run_host -- the whole single-GPU path from HOST buffers: H2D of the
  * queries, knn_robs, (GLOBAL: local bounds = the job's bounds), alpha,
  * interpolate, D2H of Z; synchronises `stream` and reports deferred errors.

@@ -44,7 +44,8 @@ EXPORTS = (
     "aidw_abi_version", "aidw_status_string", "aidw_last_error", "aidw_create", "aidw_nd",
     "aidw_area", "aidw_r_exp", "aidw_dtype_of", "aidw_knn_robs", "aidw_alpha", "aidw_interpolate",
     "aidw_run_host", "aidw_check", "aidw_launch_count", "aidw_destroy", "aidw_run_fixed", "aidw_idw",
-    "aidw_paper_baseline",
+    "aidw_paper_baseline", "aidw_set_extent", "aidw_bbox", "aidw_knn_partial", "aidw_knn_merge",
+    "aidw_interpolate_partial", "aidw_finalize",
 )
 
 
@@ -84,6 +85,12 @@ def lib():
             "aidw_run_fixed": ([P, P, P, I64, I, P, D, D, I, P, P, P, P], I),
             "aidw_idw": ([P, P, P, I64, D, P, P], I),
             "aidw_paper_baseline": ([I, I, I, P, I64, P, P, I64, I, P, D, D, D, P, P], I),
+            "aidw_set_extent": ([P, I64, D], I),
+            "aidw_bbox": ([P, P], I),
+            "aidw_knn_partial": ([P, P, P, I64, I, P, P], I),
+            "aidw_knn_merge": ([P, P, I, I64, I, P, P, P, P], I),
+            "aidw_interpolate_partial": ([P, P, P, I64, P, P, P, P], I),
+            "aidw_finalize": ([P, P, I, I64, P, P], I),
             "aidw_destroy": ([P], I),
         }
         for name, (args, res) in sig.items():
@@ -280,6 +287,42 @@ class AIDW:
         qx, qy = self._q(qx), self._q(qy)
         z = self._empty(qx.numel())
         aidw_idw(self.h, qx, qy, alpha, z, stream)
+        return z
+
+    # ---- N4: data-sharded mode (this handle holds one shard of the data points)
+    def set_extent(self, nd_total, area):
+        _err(self.h, lib().aidw_set_extent(self.h, int(nd_total), float(area)))
+        self.r_exp = lib().aidw_r_exp(self.h)
+        self.area = lib().aidw_area(self.h)
+
+    def bbox(self):
+        out = (ctypes.c_double * 4)()
+        _err(self.h, lib().aidw_bbox(self.h, out))
+        return list(out)
+
+    def knn_partial(self, qx, qy, k, stream=None):
+        qx, qy = self._q(qx), self._q(qy)
+        s = self._empty(qx.numel() * k)
+        _err(self.h, lib().aidw_knn_partial(self.h, _ptr(qx), _ptr(qy), qx.numel(), int(k), _ptr(s),
+                                            _stream(stream)))
+        return s
+
+    def knn_merge(self, lists, P, nq, k, stream=None):
+        r_obs, d1sq, mm = self._empty(nq), self._empty(nq), self._empty(2)
+        _err(self.h, lib().aidw_knn_merge(self.h, _ptr(lists), int(P), int(nq), int(k), _ptr(r_obs), _ptr(d1sq),
+                                          _ptr(mm), _stream(stream)))
+        return r_obs, d1sq, mm
+
+    def interpolate_partial(self, qx, qy, alpha, d1sq, stream=None):
+        qx, qy = self._q(qx), self._q(qy)
+        part = torch.empty(qx.numel() * 4, dtype=torch.float64, device=self.device)
+        _err(self.h, lib().aidw_interpolate_partial(self.h, _ptr(qx), _ptr(qy), qx.numel(), _ptr(alpha),
+                                                    _ptr(d1sq), _ptr(part), _stream(stream)))
+        return part
+
+    def finalize(self, partials, P, nq, stream=None):
+        z = self._empty(nq)
+        _err(self.h, lib().aidw_finalize(self.h, _ptr(partials), int(P), int(nq), _ptr(z), _stream(stream)))
         return z
 
     def run_host(self, qx_host, qy_host, k=10, levels=LEVELS_DEFAULT, rbounds=GLOBAL, r_min=0.0, r_max=2.0,

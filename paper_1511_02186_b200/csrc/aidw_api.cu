@@ -22,6 +22,7 @@ struct aidw_ctx {
     void *work = nullptr;            // run_host / internal d1sq scratch
     size_t work_bytes = 0;
     int64_t launches = 0;
+    double bbox[4] = {0, 0, 0, 0};
     char err[512] = {0};
 };
 
@@ -216,6 +217,10 @@ aidw_status aidw_create(aidw_t *out, int device, aidw_dtype dt, aidw_layout lay,
     // A: explicit, or the exact bbox (min/max exact; fp64 sub and mul) -- DESIGN.md R5
     const double x0 = decode_key(back.keys[0]), x1 = decode_key(back.keys[1]);
     const double y0 = decode_key(back.keys[2]), y1 = decode_key(back.keys[3]);
+    h->bbox[0] = x0;
+    h->bbox[1] = x1;
+    h->bbox[2] = y0;
+    h->bbox[3] = y1;
     h->area = area > 0.0 ? area : (x1 - x0) * (y1 - y0);
     if (!(h->area > 0.0) || std::isinf(h->area))
         return bail(fail(h, AIDW_E_DEGENERATE_EXTENT, "study area A = %g (bbox [%g,%g]x[%g,%g])", h->area, x0,
@@ -408,6 +413,80 @@ aidw_status aidw_paper_baseline(int variant, aidw_dtype dt, aidw_layout lay, con
                            static_cast<cudaStream_t>(stream)) < 0)
         return cuda_fail(nullptr, cudaGetLastError(), "paper baseline kernel");
     return AIDW_OK;
+}
+
+aidw_status aidw_set_extent(aidw_t h, int64_t nd_total, double area)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    if (nd_total < 1) return fail(h, AIDW_E_INVALID_ARG, "nd_total must be >= 1");
+    if (!(area > 0.0) || std::isinf(area)) return fail(h, AIDW_E_INVALID_AREA, "area = %g must be > 0", area);
+    h->area = area;
+    h->r_exp = 1.0 / (2.0 * std::sqrt((double)nd_total / area));  // Eq. 2
+    return AIDW_OK;
+}
+
+aidw_status aidw_bbox(aidw_t h, double *out)
+{
+    if (!h || !out) return fail(h, AIDW_E_INVALID_ARG, "NULL argument");
+    for (int i = 0; i < 4; ++i) out[i] = h->bbox[i];
+    return AIDW_OK;
+}
+
+aidw_status aidw_knn_partial(aidw_t h, const void *qx, const void *qy, int64_t nq, int k, void *s_out, void *stream)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    if (nq < 0) return fail(h, AIDW_E_INVALID_ARG, "nq < 0");
+    if (k < 1) return fail(h, AIDW_E_INVALID_ARG, "k = %d must be >= 1", k);
+    if (k > AIDW_KMAX) return fail(h, AIDW_E_UNSUPPORTED, "k = %d > AIDW_KMAX", k);
+    if (h->nd < k) return fail(h, AIDW_E_INSUFFICIENT_DATA, "shard nd = %lld < k = %d", (long long)h->nd, k);
+    if (nq == 0) return AIDW_OK;
+    if (!qx || !qy || !s_out) return fail(h, AIDW_E_INVALID_ARG, "NULL argument");
+    CK(h, cudaSetDevice(h->device));
+    return launched(h,
+                    aidw::launch_knn((int)h->dt, k, h->data, h->ndp, qx, qy, nq, nullptr, nullptr, nullptr, s_out,
+                                     h->sc, &h->filt, static_cast<cudaStream_t>(stream), 1),
+                    "knn partial kernel");
+}
+
+aidw_status aidw_knn_merge(aidw_t h, const void *lists, int P, int64_t nq, int k, void *r_obs, void *d1sq,
+                           void *robs_minmax, void *stream)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    if (P < 1 || nq < 0 || k < 1 || k > AIDW_KMAX) return fail(h, AIDW_E_INVALID_ARG, "bad P/nq/k");
+    CK(h, cudaSetDevice(h->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (nq == 0) {
+        if (robs_minmax) return launched(h, aidw::launch_minmax_identity((int)h->dt, robs_minmax, st), "minmax");
+        return AIDW_OK;
+    }
+    if (!lists) return fail(h, AIDW_E_INVALID_ARG, "lists is NULL");
+    return launched(h, aidw::launch_knn_merge((int)h->dt, k, lists, P, nq, r_obs, d1sq, robs_minmax, h->sc, st),
+                    "knn merge kernel");
+}
+
+aidw_status aidw_interpolate_partial(aidw_t h, const void *qx, const void *qy, int64_t nq, const void *alpha,
+                                     const void *d1sq, double *partial_out, void *stream)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    if (nq < 0) return fail(h, AIDW_E_INVALID_ARG, "nq < 0");
+    if (nq == 0) return AIDW_OK;
+    if (!qx || !qy || !alpha || !d1sq || !partial_out) return fail(h, AIDW_E_INVALID_ARG, "NULL argument");
+    CK(h, cudaSetDevice(h->device));
+    return launched(h,
+                    aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, alpha, 0.0, d1sq, nullptr,
+                                        static_cast<cudaStream_t>(stream), partial_out),
+                    "interpolate partial kernel");
+}
+
+aidw_status aidw_finalize(aidw_t h, const double *partials, int P, int64_t nq, void *z_out, void *stream)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    if (P < 1 || nq < 0) return fail(h, AIDW_E_INVALID_ARG, "bad P/nq");
+    if (nq == 0) return AIDW_OK;
+    if (!partials || !z_out) return fail(h, AIDW_E_INVALID_ARG, "NULL argument");
+    CK(h, cudaSetDevice(h->device));
+    return launched(h, aidw::launch_finalize((int)h->dt, partials, P, nq, z_out, static_cast<cudaStream_t>(stream)),
+                    "finalize kernel");
 }
 
 aidw_status aidw_check(aidw_t h, void *stream)

@@ -43,7 +43,12 @@ int launch_prep(int dtype, int layout, const void *src, int64_t nd, int64_t ndp,
 
 int launch_knn(int dtype, int k, const void *data, int64_t ndp, const void *qx, const void *qy,
                int64_t nq, void *r_obs, void *d1sq, void *minmax, void *dists, Scratch *sc,
-               const FilterData *filt, cudaStream_t st);
+               const FilterData *filt, cudaStream_t st, int dists_sq = 0);
+
+int launch_knn_merge(int dtype, int k, const void *lists, int P, int64_t nq, void *r_obs, void *d1sq,
+                     void *minmax, Scratch *sc, cudaStream_t st);
+
+int launch_finalize(int dtype, const double *partials, int P, int64_t nq, void *z, cudaStream_t st);
 
 int launch_center(const void *data, int64_t ndp, int64_t nd, float c_x, float c_y, void *filt,
                   cudaStream_t st);
@@ -62,9 +67,11 @@ int launch_paper(int variant, int dtype, int layout, const void *data, int64_t n
                  int64_t nq, int k, double r_exp, const double *lv, double rmin, double rmax, void *z,
                  cudaStream_t st);
 
-// alpha == nullptr -> every query uses alpha_const (standard IDW, Eq. 1 with a constant power)
+// alpha == nullptr -> every query uses alpha_const (standard IDW, Eq. 1 with a constant power).
+// partial != nullptr -> write per-query fp64 {sum w, sum w z, sum z_coincident, n_coincident}
+// over this handle's data (data-sharded mode) instead of z.
 int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const void *qx,
                   const void *qy, int64_t nq, const void *alpha, double alpha_const, const void *d1sq, void *z,
-                  cudaStream_t st);
+                  cudaStream_t st, double *partial = nullptr);
 
 }  // namespace aidw

@@ -26,6 +26,7 @@ template <typename T> struct InterpArgs {
     int64_t nq;
     T *z;
     T alpha_const;
+    double *partial;  // nullable: data-sharded partial sums instead of z
 };
 
 __device__ __forceinline__ float wlog2(float s) { return lg2_approx(s); }
@@ -120,13 +121,10 @@ __global__ void __launch_bounds__(kBlock) interp_kernel(const InterpArgs<T> a)
     }
 
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        if (!valid[q]) continue;
-        const int64_t idx = base + q * kBlock;
-        double zq = SWZ[q] / SW[q];
-        if (d1[q] == T(0)) zq = coincident_mean<T>(qx[q], qy[q], a.px, a.py, a.pz, a.nd);  // R19
-        a.z[idx] = (T)zq;
-    }
+    for (int q = 0; q < Q; ++q)
+        if (valid[q])
+            write_result<T>(a.z, a.partial, base + q * kBlock, SW[q], SWZ[q], d1[q], qx[q], qy[q], a.px, a.py,
+                            a.pz, a.nd);
 }
 
 // Packed fp32 kernel (passes.cuh interp_f32_tile).
@@ -165,13 +163,10 @@ __global__ void __launch_bounds__(kBlock) interp_f32x2_kernel(const InterpArgs<f
     }
 
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        if (!valid[q]) continue;
-        const int64_t idx = base + q * kBlock;
-        double zq = st.SWZ[q] / st.SW[q];
-        if (d1[q] == 0.f) zq = coincident_mean<float>(qx[q], qy[q], a.px, a.py, a.pz, a.nd);  // R19
-        a.z[idx] = (float)zq;
-    }
+    for (int q = 0; q < Q; ++q)
+        if (valid[q])
+            write_result<float>(a.z, a.partial, base + q * kBlock, st.SW[q], st.SWZ[q], d1[q], qx[q], qy[q], a.px,
+                                a.py, a.pz, a.nd);
 }
 
 template <typename T, int Q>
@@ -227,19 +222,48 @@ static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st)
     }
 }
 
+// N4: Z from P shards' partials [P][nq][4], summed in rank order (deterministic).
+template <typename T>
+__global__ void finalize_kernel(const double *__restrict__ part, int P, int64_t nq, T *__restrict__ z)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
+        double sw = 0.0, swz = 0.0, zc = 0.0, nc = 0.0;
+        for (int p = 0; p < P; ++p) {
+            const double *r = part + 4 * ((int64_t)p * nq + i);
+            sw += r[0];
+            swz += r[1];
+            zc += r[2];
+            nc += r[3];
+        }
+        z[i] = (T)(nc > 0.0 ? zc / nc : swz / sw);
+    }
+}
+
+int launch_finalize(int dtype, const double *partials, int P, int64_t nq, void *z, cudaStream_t st)
+{
+    int64_t blocks = (nq + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (dtype == 0)
+        finalize_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(partials, P, nq, (float *)z);
+    else
+        finalize_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(partials, P, nq, (double *)z);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
 int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const void *qx,
                   const void *qy, int64_t nq, const void *alpha, double alpha_const, const void *d1sq, void *z,
-                  cudaStream_t st)
+                  cudaStream_t st, double *partial)
 {
     if (dtype == 0) {
         const float *p = static_cast<const float *>(data);
         InterpArgs<float> a{p, p + ndp, p + 2 * ndp, ndp, nd, (const float *)qx, (const float *)qy,
-                            (const float *)alpha, (const float *)d1sq, nq, (float *)z, (float)alpha_const};
+                            (const float *)alpha, (const float *)d1sq, nq, (float *)z, (float)alpha_const,
+                            partial};
         return launch_interp_f32(a, st);
     }
     const double *p = static_cast<const double *>(data);
     InterpArgs<double> a{p, p + ndp, p + 2 * ndp, ndp, nd, (const double *)qx, (const double *)qy,
-                         (const double *)alpha, (const double *)d1sq, nq, (double *)z, alpha_const};
+                         (const double *)alpha, (const double *)d1sq, nq, (double *)z, alpha_const, partial};
     return launch_interp_t<double, 2>(a, st);
 }
 

@@ -33,8 +33,9 @@ template <typename T> struct KnnArgs {
     const T *qx, *qy;
     int64_t nq;
     int k;
-    T *r_obs, *d1sq, *minmax, *dists;
+    T *r_obs, *d1sq, *minmax, *dists;  // all nullable except where the caller needs them
     Scratch *sc;
+    int dists_sq;  // 1: dists receives the k squared distances s (data-sharded partial lists)
 };
 
 template <typename T> __device__ __forceinline__ T from_bits(unsigned long long b);
@@ -96,13 +97,13 @@ __device__ __forceinline__ void knn_epilogue(const KnnArgs<T> &a, T (&buf)[Q][K]
         robs_l[q] = robs;
         const int64_t idx = base + q * kBlock;
         if (valid[q]) {
-            a.r_obs[idx] = robs;
+            if (a.r_obs) a.r_obs[idx] = robs;
             if (a.d1sq) a.d1sq[idx] = d1;
             if (a.dists) {
                 T *o = a.dists + idx * a.k;
 #pragma unroll
                 for (int i = 0; i < K; ++i)
-                    if (i >= k0) o[i - k0] = sqrt_rn(buf[q][i]);
+                    if (i >= k0) o[i - k0] = a.dists_sq ? buf[q][i] : sqrt_rn(buf[q][i]);
             }
         }
     }
@@ -307,6 +308,69 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
     return launch_knn_filter_t<32, 2>(a, f, st);
 }
 
+// ---------------------------------------------------------------------------------
+// N4 (data-sharded mode): merge P per-shard lists of the k smallest squared distances
+// (each ascending, layout [P][nq][k]) into the job's k smallest -- the same register
+// top-K insertion, so the merged multiset, r_obs and d1sq are bit-identical to a
+// single-device run over the whole data -- then the usual epilogue.
+template <typename T, int K>
+__global__ void __launch_bounds__(kBlock) knn_merge_kernel(const KnnArgs<T> a, const T *__restrict__ lists, int P)
+{
+    constexpr int Q = 1;
+    const int64_t base = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    bool valid[Q] = {base < a.nq};
+    T buf[Q][K];
+    const int k0 = K - a.k;
+#pragma unroll
+    for (int i = 0; i < K; ++i) buf[0][i] = (i < k0) ? -pos_inf<T>() : pos_inf<T>();
+    if (valid[0])
+        for (int p = 0; p < P; ++p) {
+            const T *l = lists + ((int64_t)p * a.nq + base) * a.k;
+            for (int i = 0; i < a.k; ++i) {
+                const T s = l[i];
+                if (s < buf[0][K - 1]) topk_insert<T, K>(buf[0], s);
+            }
+        }
+    knn_epilogue<T, K, Q>(a, buf, valid, base, k0);
+}
+
+template <typename T, int K>
+static int launch_merge_k(const KnnArgs<T> &a, const T *lists, int P, cudaStream_t st)
+{
+    const unsigned grid = (unsigned)((a.nq + kBlock - 1) / kBlock);
+    knn_merge_kernel<T, K><<<grid, kBlock, 0, st>>>(a, lists, P);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+template <typename T>
+static int dispatch_merge(const KnnArgs<T> &a, const T *lists, int P, cudaStream_t st)
+{
+    const int k = a.k;
+    if (k <= 1) return launch_merge_k<T, 1>(a, lists, P, st);
+    if (k <= 2) return launch_merge_k<T, 2>(a, lists, P, st);
+    if (k <= 4) return launch_merge_k<T, 4>(a, lists, P, st);
+    if (k <= 8) return launch_merge_k<T, 8>(a, lists, P, st);
+    if (k <= 10) return launch_merge_k<T, 10>(a, lists, P, st);
+    if (k <= 12) return launch_merge_k<T, 12>(a, lists, P, st);
+    if (k <= 15) return launch_merge_k<T, 15>(a, lists, P, st);
+    if (k <= 16) return launch_merge_k<T, 16>(a, lists, P, st);
+    if (k <= 24) return launch_merge_k<T, 24>(a, lists, P, st);
+    return launch_merge_k<T, 32>(a, lists, P, st);
+}
+
+int launch_knn_merge(int dtype, int k, const void *lists, int P, int64_t nq, void *r_obs, void *d1sq,
+                     void *minmax, Scratch *sc, cudaStream_t st)
+{
+    if (dtype == 0) {
+        KnnArgs<float> a{nullptr, nullptr, 0, nullptr, nullptr, nq, k, (float *)r_obs, (float *)d1sq,
+                         (float *)minmax, nullptr, sc, 0};
+        return dispatch_merge(a, (const float *)lists, P, st);
+    }
+    KnnArgs<double> a{nullptr, nullptr, 0, nullptr, nullptr, nq, k, (double *)r_obs, (double *)d1sq,
+                      (double *)minmax, nullptr, sc, 0};
+    return dispatch_merge(a, (const double *)lists, P, st);
+}
+
 template <typename T> __global__ void minmax_identity_kernel(T *mm)
 {
     mm[0] = -pos_inf<T>();
@@ -344,12 +408,12 @@ static int dispatch_k(const KnnArgs<T> &a, cudaStream_t st)
 
 int launch_knn(int dtype, int k, const void *data, int64_t ndp, const void *qx, const void *qy,
                int64_t nq, void *r_obs, void *d1sq, void *minmax, void *dists, Scratch *sc,
-               const FilterData *filt, cudaStream_t st)
+               const FilterData *filt, cudaStream_t st, int dists_sq)
 {
     if (dtype == 0) {
         const float *p = static_cast<const float *>(data);
         KnnArgs<float> a{p, p + ndp, ndp, (const float *)qx, (const float *)qy, nq, k,
-                         (float *)r_obs, (float *)d1sq, (float *)minmax, (float *)dists, sc};
+                         (float *)r_obs, (float *)d1sq, (float *)minmax, (float *)dists, sc, dists_sq};
         if (filt && filt->arrays) {
             const float *c = static_cast<const float *>(filt->arrays);
             FilterArgs f{c, c + ndp, c + 2 * ndp, filt->c_x, filt->c_y, filt->r1};
@@ -359,7 +423,7 @@ int launch_knn(int dtype, int k, const void *data, int64_t ndp, const void *qx, 
     }
     const double *p = static_cast<const double *>(data);
     KnnArgs<double> a{p, p + ndp, ndp, (const double *)qx, (const double *)qy, nq, k,
-                      (double *)r_obs, (double *)d1sq, (double *)minmax, (double *)dists, sc};
+                      (double *)r_obs, (double *)d1sq, (double *)minmax, (double *)dists, sc, dists_sq};
     return dispatch_k(a, st);
 }
 

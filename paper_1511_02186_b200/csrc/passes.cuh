@@ -317,16 +317,42 @@ __device__ __forceinline__ void interp_f32_tile(InterpF32State<Q> &st, const flo
 // Exact coincidence (R19): the limit of Eq. 1 is the mean z of the data points at
 // distance 0.  Rare; one extra pass over global memory for the calling lane.
 template <typename T>
-__device__ __forceinline__ double coincident_mean(T qx, T qy, const T *px, const T *py, const T *pz, int64_t nd)
+__device__ __forceinline__ void coincident_sums(T qx, T qy, const T *px, const T *py, const T *pz, int64_t nd,
+                                                double &zc, double &cnt)
 {
-    double zc = 0.0;
-    long long cnt = 0;
+    zc = 0.0;
+    cnt = 0.0;
     for (int64_t i = 0; i < nd; ++i)
         if (dist_sq(qx, qy, px[i], py[i]) == T(0)) {
             zc += (double)pz[i];
-            ++cnt;
+            cnt += 1.0;
         }
-    return zc / (double)cnt;
+}
+
+template <typename T>
+__device__ __forceinline__ double coincident_mean(T qx, T qy, const T *px, const T *py, const T *pz, int64_t nd)
+{
+    double zc, cnt;
+    coincident_sums<T>(qx, qy, px, py, pz, nd, zc, cnt);
+    return zc / cnt;
+}
+
+// Per-query result: Z (Eq. 1, or the coincidence mean R19), or -- in data-sharded mode --
+// this shard's fp64 partials {sum w, sum w z, sum z_coincident, n_coincident}.
+template <typename T>
+__device__ __forceinline__ void write_result(T *z, double *partial, int64_t idx, double SW, double SWZ, T d1, T qx,
+                                             T qy, const T *px, const T *py, const T *pz, int64_t nd)
+{
+    double zc = 0.0, nc = 0.0;
+    if (d1 == T(0)) coincident_sums<T>(qx, qy, px, py, pz, nd, zc, nc);
+    if (partial) {
+        partial[4 * idx] = SW;
+        partial[4 * idx + 1] = SWZ;
+        partial[4 * idx + 2] = zc;
+        partial[4 * idx + 3] = nc;
+    } else {
+        z[idx] = (T)(d1 == T(0) ? zc / nc : SWZ / SW);
+    }
 }
 
 }  // namespace aidw

@@ -50,6 +50,61 @@ def run_sharded(engine, qx, qy, k, levels, rbounds=GLOBAL, r_min=0.0, r_max=2.0,
     return engine.interpolate(qx, qy, a, d1sq)
 
 
+# ---------------------------------------------------------------------------------
+# N4: data-sharded mode.  The DATA points are split across ranks (shard boundaries at
+# multiples of `align` points so the fp32 tile sums are the single-device ones); every
+# rank evaluates ALL queries against its shard.  Exchanges per run: one all-gather of the
+# k smallest squared distances (k * nq values per rank) and one all-gather of the Eq. 1
+# partial sums (4 fp64 per query per rank); both are reduced in rank order on the device
+# (aidw_knn_merge, aidw_finalize), so results are deterministic for a given world size.
+# The merged kNN lists, r_obs, the GLOBAL R bounds and alpha are bit-identical to one
+# device; Z differs from it only in the fp64 order of the cross-shard sum.
+
+def data_shard(nd: int, rank: int, world: int, align: int = 1024) -> tuple[int, int]:
+    """[start, end) of the data points of `rank`; interior boundaries are multiples of align."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    blocks = (nd + align - 1) // align
+    s, e = shard(blocks, rank, world)
+    return min(nd, s * align), min(nd, e * align)
+
+
+def global_extent(engine, group=None):
+    """(nd_total, area) of the whole data set from every rank's shard (Eq. 2 inputs)."""
+    x0, x1, y0, y1 = engine.bbox()
+    dev = getattr(engine, "device", torch.device("cpu"))
+    t = torch.tensor([-x0, x1, -y0, y1], dtype=torch.float64, device=dev)
+    n = torch.tensor([float(engine.nd)], dtype=torch.float64, device=dev)
+    if group is not None and dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        dist.all_reduce(n, op=dist.ReduceOp.SUM, group=group)
+    t = t.cpu()
+    return int(n.item()), float((t[1] + t[0]) * (t[3] + t[2]))
+
+
+def _all_gather_cat(x: torch.Tensor, group=None) -> torch.Tensor:
+    world = dist.get_world_size(group) if group is not None and dist.is_initialized() else 1
+    if world == 1:
+        return x
+    parts = [torch.empty_like(x) for _ in range(world)]
+    dist.all_gather(parts, x.contiguous(), group=group)
+    return torch.cat(parts)
+
+
+def run_data_sharded(engine, qx, qy, k, levels, rbounds=GLOBAL, r_min=0.0, r_max=2.0, muform=0, group=None):
+    """Full AIDW with the data split across ranks; every rank returns Z for ALL queries.
+    `engine` holds this rank's data shard with the global extent set (global_extent)."""
+    world = dist.get_world_size(group) if group is not None and dist.is_initialized() else 1
+    nq = len(qx)
+    s_local = engine.knn_partial(qx, qy, k)
+    lists = _all_gather_cat(s_local, group)
+    r_obs, d1sq, mm = engine.knn_merge(lists, world, nq, k)  # mm already covers all queries
+    a = engine.alpha(r_obs, levels, rbounds, r_min, r_max, mm, muform)
+    part = engine.interpolate_partial(qx, qy, a, d1sq)
+    parts = _all_gather_cat(part, group)
+    return engine.finalize(parts, world, nq)
+
+
 def gather(z_local: torch.Tensor, nq: int, group=None) -> torch.Tensor:
     """Optional all-gather of the per-rank Z blocks into the full [nq] result."""
     world = dist.get_world_size(group)

@@ -358,3 +358,37 @@ def test_paper_baseline_kernels(P, orc, dtype, variant):
         P.aidw_paper_baseline(variant, t(buf), len(x), t(qx), t(qy), 10, LV, area, 0.0, 2.0, zo, lay)
         torch.cuda.synchronize()
         assert rel_err(zo.cpu().numpy(), Zo).max() <= (1e-3 if dtype == torch.float32 else 1e-10)
+
+
+# ------------------------------------------------------------------ N4: data sharding
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_data_sharded_emulated(P, orc, dtype):
+    """Data split over 1..4 'ranks' (handles on one device): merged kNN lists, r_obs,
+    d1sq, the GLOBAL bounds and alpha are bit-identical to one handle over all data; Z
+    differs only in the fp64 order of the cross-shard sum."""
+    from paper_1511_02186_b200.partition import data_shard
+    x, y, z, qx, qy = datagen.random_cloud(88, 9000, 1500)
+    qx = np.concatenate([qx, x[[5, 4000, 8999]]])  # coincident queries in different shards
+    qy = np.concatenate([qy, y[[5, 4000, 8999]]])
+    nq = len(qx)
+    full = P.AIDW(x, y, z, dtype=dtype)
+    r0, d0, m0 = full.knn_robs(qx, qy, 10)
+    z0 = full.run(qx, qy, 10, LV, P.GLOBAL)
+    Zo = orc.aidw(x, y, z, qx, qy, 10, LV, mode="global")
+    for world in (1, 2, 3, 4):
+        engs = []
+        for r in range(world):
+            s, e = data_shard(len(x), r, world)
+            eng = P.AIDW(x[s:e], y[s:e], z[s:e], dtype=dtype)
+            eng.set_extent(len(x), full.area)
+            engs.append(eng)
+        lists = torch.cat([eng.knn_partial(qx, qy, 10) for eng in engs])
+        r_obs, d1, mm = engs[0].knn_merge(lists, world, nq, 10)
+        assert torch.equal(r_obs, r0) and torch.equal(d1, d0) and torch.equal(mm, m0), world
+        a = engs[0].alpha(r_obs, LV, P.GLOBAL, 0, 0, mm)
+        parts = torch.cat([eng.interpolate_partial(qx, qy, a, d1) for eng in engs])
+        zw = engs[0].finalize(parts, world, nq)
+        if world == 1:
+            assert torch.equal(zw, z0)
+        assert rel_err(zw.cpu().numpy(), z0.cpu().numpy().astype(np.float64)).max() <= 1e-6
+        assert rel_err(zw.cpu().numpy(), Zo).max() <= TOL[dtype]
