@@ -293,17 +293,22 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
         switch (knn_variant()) {  // tuning sweep (tools/tune_knn.py)
         case 2: return launch_knn_filter_t<10, 4, 8>(a, f, st);
         case 3: return launch_knn_filter_t<10, 2, 16>(a, f, st);
+        case 4: return launch_knn_filter_t<10, 2, 8>(a, f, st);
+        case 5: return launch_knn_filter_t<10, 3, 16>(a, f, st);
+        case 6: return launch_knn_filter_t<10, 4, 16>(a, f, st);
+        case 7: return launch_knn_filter_t<10, 2, 32>(a, f, st);
         default: break;
         }
     }
-    if (k <= 1) return launch_knn_filter_t<1, 2>(a, f, st);
-    if (k <= 2) return launch_knn_filter_t<2, 2>(a, f, st);
-    if (k <= 4) return launch_knn_filter_t<4, 2>(a, f, st);
-    if (k <= 8) return launch_knn_filter_t<8, 2>(a, f, st);
-    if (k <= 10) return launch_knn_filter_t<10, 2>(a, f, st);
-    if (k <= 12) return launch_knn_filter_t<12, 2>(a, f, st);
-    if (k <= 15) return launch_knn_filter_t<15, 2>(a, f, st);
-    if (k <= 16) return launch_knn_filter_t<16, 2>(a, f, st);
+    // Q = 2 queries per thread, G = 16 points per warp vote (best measured, r01)
+    if (k <= 1) return launch_knn_filter_t<1, 2, 16>(a, f, st);
+    if (k <= 2) return launch_knn_filter_t<2, 2, 16>(a, f, st);
+    if (k <= 4) return launch_knn_filter_t<4, 2, 16>(a, f, st);
+    if (k <= 8) return launch_knn_filter_t<8, 2, 16>(a, f, st);
+    if (k <= 10) return launch_knn_filter_t<10, 2, 16>(a, f, st);
+    if (k <= 12) return launch_knn_filter_t<12, 2, 16>(a, f, st);
+    if (k <= 15) return launch_knn_filter_t<15, 2, 16>(a, f, st);
+    if (k <= 16) return launch_knn_filter_t<16, 2, 16>(a, f, st);
     if (k <= 24) return launch_knn_filter_t<24, 2>(a, f, st);
     return launch_knn_filter_t<32, 2>(a, f, st);
 }

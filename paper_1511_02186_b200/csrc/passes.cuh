@@ -130,43 +130,41 @@ struct KnnF32State {
     }
 };
 
-// One smem tile of TILE points: filter values in groups of G points per warp vote;
-// the next group's smem loads are issued right after the current group's filter
-// values are formed, so they overlap the vote; a bitmask rare path re-checks only the
-// passing pairs with the canonical distance.
+// One smem tile of TILE points: filter values in groups of G points per warp vote
+// (loaded in chunks of 8 points, so only one chunk's inputs are live at a time); a
+// bitmask rare path re-checks only the passing pairs with the canonical distance.
 template <int K, int Q, int G, int TILE>
 __device__ __forceinline__ void knn_f32_tile(KnnF32State<K, Q> &st, const float *__restrict__ tcx,
                                              const float *__restrict__ tcy, const float *__restrict__ tpp,
                                              const float *__restrict__ tpx, const float *__restrict__ tpy)
 {
-    static_assert(G % 4 == 0 && G <= 32 && TILE % G == 0, "group size");
-    float cxv[G], cyv[G], ppv[G];
-    auto load = [&](int j) {
-#pragma unroll
-        for (int g = 0; g < G; g += 4) {
-            const float4 CX = *reinterpret_cast<const float4 *>(tcx + j + g);
-            const float4 CY = *reinterpret_cast<const float4 *>(tcy + j + g);
-            const float4 PP = *reinterpret_cast<const float4 *>(tpp + j + g);
-            cxv[g] = CX.x; cxv[g + 1] = CX.y; cxv[g + 2] = CX.z; cxv[g + 3] = CX.w;
-            cyv[g] = CY.x; cyv[g + 1] = CY.y; cyv[g + 2] = CY.z; cyv[g + 3] = CY.w;
-            ppv[g] = PP.x; ppv[g + 1] = PP.y; ppv[g + 2] = PP.z; ppv[g + 3] = PP.w;
-        }
-    };
-    load(0);
+    static_assert(G % 8 == 0 && G <= 32 && TILE % G == 0, "group size");
 #pragma unroll 1
     for (int j = 0; j < TILE; j += G) {
         float tv[Q][G];
 #pragma unroll
-        for (int q = 0; q < Q; ++q)
+        for (int c = 0; c < G; c += 8) {
+            float cxv[8], cyv[8], ppv[8];
 #pragma unroll
-            for (int h = 0; h < G / 2; ++h) {
-                const f32x2 tt = fma2(splat2(st.B[q]), pack2(cyv[2 * h], cyv[2 * h + 1]),
-                                      fma2(splat2(st.A[q]), pack2(cxv[2 * h], cxv[2 * h + 1]),
-                                           pack2(ppv[2 * h], ppv[2 * h + 1])));
-                tv[q][2 * h] = tt.x;
-                tv[q][2 * h + 1] = tt.y;
+            for (int g = 0; g < 8; g += 4) {
+                const float4 CX = *reinterpret_cast<const float4 *>(tcx + j + c + g);
+                const float4 CY = *reinterpret_cast<const float4 *>(tcy + j + c + g);
+                const float4 PP = *reinterpret_cast<const float4 *>(tpp + j + c + g);
+                cxv[g] = CX.x; cxv[g + 1] = CX.y; cxv[g + 2] = CX.z; cxv[g + 3] = CX.w;
+                cyv[g] = CY.x; cyv[g + 1] = CY.y; cyv[g + 2] = CY.z; cyv[g + 3] = CY.w;
+                ppv[g] = PP.x; ppv[g + 1] = PP.y; ppv[g + 2] = PP.z; ppv[g + 3] = PP.w;
             }
-        load(j + G < TILE ? j + G : j);
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const f32x2 tt = fma2(splat2(st.B[q]), pack2(cyv[2 * h], cyv[2 * h + 1]),
+                                          fma2(splat2(st.A[q]), pack2(cxv[2 * h], cxv[2 * h + 1]),
+                                               pack2(ppv[2 * h], ppv[2 * h + 1])));
+                    tv[q][c + 2 * h] = tt.x;
+                    tv[q][c + 2 * h + 1] = tt.y;
+                }
+        }
         bool hit = false;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
