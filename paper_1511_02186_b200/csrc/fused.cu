@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kBlock) fused_fixed_kernel(const FusedArgs a)
     }
 }
 
-template <int K, int Q = 2, int G = 16, unsigned EMU = 0x19>
+template <int K, int Q = 2, int G = 16, unsigned EMU = 0x0141>
 static int launch_fused_t(const FusedArgs &a, cudaStream_t st)
 {
     const size_t smem = (size_t)5 * kStagesKF * kTileKF * sizeof(float) + 2 * kStagesKF * sizeof(uint64_t);

@@ -208,17 +208,17 @@ static int interp_variant()
 
 static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st)
 {
-    // EMU: bit 2g+h = couple h of 4-point group g (of 16) on the FMA pipe
+    // EMU: 2-bit mode per couple h of 4-point group g at bit 4g+2h (passes.cuh)
     switch (interp_variant()) {
-    case 1: return launch_interp_t<float, 2>(a, st);      // scalar, all-SFU
-    case 2: return launch_interp_f32x2<2, 0x00>(a, st);   // packed, all-SFU
-    case 3: return launch_interp_f32x2<2, 0x55>(a, st);   // 4 of 8 couples on the FMA pipe
-    case 4: return launch_interp_f32x2<2, 0x11>(a, st);   // 2 of 8
-    case 5: return launch_interp_f32x2<2, 0xFF>(a, st);   // all on the FMA pipe
-    case 6: return launch_interp_f32x2<2, 0x59>(a, st);   // 4 of 8, spread h
-    case 7: return launch_interp_f32x2<4, 0x19>(a, st);   // Q=4, 3 of 8
-    case 8: return launch_interp_f32x2<2, 0x5D>(a, st);   // 5 of 8
-    default: return launch_interp_f32x2<2, 0x19>(a, st);  // 3 of 8 (best measured, r01)
+    case 1: return launch_interp_t<float, 2>(a, st);        // scalar, all-SFU
+    case 2: return launch_interp_f32x2<2, 0x0000>(a, st);   // packed, all-SFU
+    case 3: return launch_interp_f32x2<2, 0x1111>(a, st);   // 4 of 8 couples on the FMA pipe
+    case 4: return launch_interp_f32x2<2, 0xAAAA>(a, st);   // every couple split (f = 1/2)
+    case 5: return launch_interp_f32x2<2, 0x2A2A>(a, st);   // f = 3/8, split
+    case 6: return launch_interp_f32x2<2, 0x2222>(a, st);   // f = 1/4, split
+    case 7: return launch_interp_f32x2<2, 0x22A2>(a, st);   // f = 5/16, split
+    case 8: return launch_interp_f32x2<2, 0x1241>(a, st);   // f = 3/8, packed + one split
+    default: return launch_interp_f32x2<2, 0x0141>(a, st); // f = 3/8 packed (best measured, r01)
     }
 }
 

@@ -49,4 +49,19 @@ __device__ __forceinline__ f32x2 exp2_poly2(f32x2 a)
     return pack2(r0, r1);
 }
 
+// Scalar form of exp2_poly2 (same constants and operation order, per element).
+__device__ __forceinline__ float exp2_poly1(float a)
+{
+    constexpr float kMagic = 12582912.0f;
+    const float x = fmaxf(a, -126.0f);
+    const float t = __fadd_rn(x, kMagic);
+    const float j = __fadd_rn(t, -kMagic);
+    const float f = __fadd_rn(x, -j);
+    float p = __fmaf_rn(0.009570101276040077f, f, 0.05591785907745361f);
+    p = __fmaf_rn(p, f, 0.240247443318367f);
+    p = __fmaf_rn(p, f, 0.6931217908859253f);
+    p = __fmaf_rn(p, f, 0.9999992847442627f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 }  // namespace aidw

@@ -273,8 +273,11 @@ __device__ __forceinline__ void interp_f32_group(InterpF32State<Q> &st, f32x2 (&
             const f32x2 l = pack2(lg2_approx(s.x), lg2_approx(s.y));
             const f32x2 e = fma2(st.C[q], l, st.B[q]);
             f32x2 w;
-            if (HMASK & (1u << h))
-                w = exp2_poly2(e);
+            const unsigned m = (HMASK >> (2 * h)) & 3u;
+            if (m == 1u)
+                w = exp2_poly2(e);  // both lanes on the FMA pipe (packed)
+            else if (m == 2u)
+                w = pack2(ex2_approx(e.x), exp2_poly1(e.y));  // split: SFU + FMA pipe
             else
                 w = pack2(ex2_approx(e.x), ex2_approx(e.y));
             sw[q] = add2(sw[q], w);
@@ -285,9 +288,10 @@ __device__ __forceinline__ void interp_f32_group(InterpF32State<Q> &st, f32x2 (&
 // One smem tile of the fp32 weighting pass with packed fp32x2 arithmetic.  Two
 // consecutive data points of one query form a "couple" in one register pair; the fp32
 // tile sums are {even, odd} partial sums folded into fp64 at the end of the tile (R21).
-// The exp2 of couple h of 4-point group g (g = 0..3 within each 16 points) runs on the
-// FMA pipe (exp2_poly2) when bit 2g+h of EMU is set, on the SFU otherwise (DESIGN.md
-// §4.3).  The choice depends on the data-point index only -- never on which register
+// The exp2 of couple h of 4-point group g (g = 0..3 within each 16 points) is chosen by
+// the 2-bit field at bit 4g+2h of EMU: 0 = both lanes on the SFU, 1 = both on the FMA
+// pipe (packed polynomial), 2 = split (lane x on the SFU, lane y on the FMA pipe)
+// (DESIGN.md §4.3).  The choice depends on the data-point index only -- never on which register
 // slot holds the query -- so every query's rounding is independent of its position in
 // the launch (bit-identical results for any sharding).
 template <int Q, unsigned EMU, int TILE>
@@ -300,10 +304,10 @@ __device__ __forceinline__ void interp_f32_tile(InterpF32State<Q> &st, const flo
     for (int q = 0; q < Q; ++q) sw[q] = swz[q] = make_float2(0.f, 0.f);
 #pragma unroll 1
     for (int j = 0; j < TILE; j += 16) {
-        interp_f32_group<Q, (EMU >> 0) & 3u>(st, sw, swz, tx + j, ty + j, tz + j);
-        interp_f32_group<Q, (EMU >> 2) & 3u>(st, sw, swz, tx + j + 4, ty + j + 4, tz + j + 4);
-        interp_f32_group<Q, (EMU >> 4) & 3u>(st, sw, swz, tx + j + 8, ty + j + 8, tz + j + 8);
-        interp_f32_group<Q, (EMU >> 6) & 3u>(st, sw, swz, tx + j + 12, ty + j + 12, tz + j + 12);
+        interp_f32_group<Q, (EMU >> 0) & 15u>(st, sw, swz, tx + j, ty + j, tz + j);
+        interp_f32_group<Q, (EMU >> 4) & 15u>(st, sw, swz, tx + j + 4, ty + j + 4, tz + j + 4);
+        interp_f32_group<Q, (EMU >> 8) & 15u>(st, sw, swz, tx + j + 8, ty + j + 8, tz + j + 8);
+        interp_f32_group<Q, (EMU >> 12) & 15u>(st, sw, swz, tx + j + 12, ty + j + 12, tz + j + 12);
     }
 #pragma unroll
     for (int q = 0; q < Q; ++q) {

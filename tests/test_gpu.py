@@ -392,3 +392,28 @@ def test_data_sharded_emulated(P, orc, dtype):
             assert torch.equal(zw, z0)
         assert rel_err(zw.cpu().numpy(), z0.cpu().numpy().astype(np.float64)).max() <= 1e-6
         assert rel_err(zw.cpu().numpy(), Zo).max() <= TOL[dtype]
+
+
+def test_C5_grid_full_size_sampled(P, orc):
+    """C5: 1M uniform data x 8,192,000 grid queries (4096 x 2000 cell centres), k = 10,
+    GLOBAL bounds, in one launch per stage: kNN + r_obs bit-exact on a strided sample, the
+    published bounds equal the min/max of the full r_obs array, sampled Z within 1e-4."""
+    x, y, z = datagen.make_data("C5")
+    qx, qy = datagen.make_queries("C5")
+    eng = P.AIDW(x, y, z)
+    tq = lambda v: torch.as_tensor(v, dtype=torch.float32, device="cuda")
+    tqx, tqy = tq(qx), tq(qy)
+    r, d1, mm = eng.knn_robs(tqx, tqy, 10)
+    a = eng.alpha(r, LV, P.GLOBAL, 0, 0, mm)
+    zg = eng.interpolate(tqx, tqy, a, d1).cpu().numpy()
+    sub = np.concatenate([np.arange(0, len(qx), 131071), [len(qx) - 1]])
+    ro = orc.knn_f32(x, y, qx[sub], qy[sub], 10)
+    rc = r.cpu().numpy()
+    assert np.array_equal(rc[sub], ro)
+    mmc = mm.cpu().numpy()
+    assert mmc[0] == -rc.min() and mmc[1] == rc.max()
+    re = eng.r_exp
+    ro64 = orc.knn_f64(x, y, qx[sub], qy[sub], 10)
+    a_o = orc.alpha(ro64, re, LV, -float(mmc[0]) / re, float(mmc[1]) / re)
+    Zo = orc.idw(x, y, z, qx[sub], qy[sub], a_o)
+    assert rel_err(zg[sub], Zo).max() <= 1e-4
