@@ -160,7 +160,7 @@ def run_reference(args):
     oracle.build()
     cores = oracle.num_threads()
     # each step: a bounded sample sized so the whole run ends within minutes
-    per_step = max(cores, int(args.ref_queries_per_step or 4 * cores))
+    per_step = max(cores, int(args.ref_queries_per_step or 32 * cores))
     times = []
     for i in range(args.warmup + args.steps):
         s = (i * per_step) % (len(qx) - per_step)
