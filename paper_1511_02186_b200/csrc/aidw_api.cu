@@ -21,6 +21,8 @@ struct aidw_ctx {
     aidw::FilterData filt;           // fp32 kNN filter arrays
     void *work = nullptr;            // run_host / internal d1sq scratch
     size_t work_bytes = 0;
+    int *perm = nullptr;             // weighting-pass class permutation (fp32)
+    int64_t perm_cap = 0;
     int64_t launches = 0;
     double bbox[4] = {0, 0, 0, 0};
     char err[512] = {0};
@@ -79,6 +81,33 @@ aidw_status ensure_work(aidw_t h, size_t bytes)
     }
     h->work_bytes = bytes;
     return AIDW_OK;
+}
+
+// Class permutation buffer for the fp32 weighting pass (nullptr: feature disabled or
+// fp64).  AIDW_ALPHA_CLASSES=0 disables the exact-exponent paths.
+int *perm_for(aidw_t h, int64_t nq)
+{
+    if (h->dt != AIDW_F32) return nullptr;
+    static int enabled = -1;
+    if (enabled < 0) {
+        const char *e = getenv("AIDW_ALPHA_CLASSES");
+        enabled = !(e && e[0] == '0');
+    }
+    if (!enabled) return nullptr;
+    if (h->perm_cap < nq) {
+        if (h->perm) {
+            cudaDeviceSynchronize();
+            cudaFree(h->perm);
+            h->perm = nullptr;
+            h->perm_cap = 0;
+        }
+        if (cudaMalloc(&h->perm, (size_t)nq * sizeof(int)) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;  // fall back to the unpermuted (general-formula) launch
+        }
+        h->perm_cap = nq;
+    }
+    return h->perm;
 }
 
 bool is_device_ptr(const void *p)
@@ -329,7 +358,8 @@ aidw_status aidw_interpolate(aidw_t h, const void *qx, const void *qy, int64_t n
         d1sq = d1;
     }
     return launched(h,
-                    aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, alpha, 0.0, d1sq, z_out, st),
+                    aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, alpha, 0.0, d1sq, z_out, st,
+                                        nullptr, perm_for(h, nq), h->sc->cls),
                     "interpolate kernel");
 }
 
@@ -390,7 +420,7 @@ aidw_status aidw_idw(aidw_t h, const void *qx, const void *qy, int64_t nq, doubl
     if (s != AIDW_OK) return s;
     return launched(h,
                     aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, nullptr, alpha, w + nb,
-                                        z_out, st),
+                                        z_out, st, nullptr, perm_for(h, nq), h->sc->cls),
                     "interpolate kernel");
 }
 
@@ -474,7 +504,8 @@ aidw_status aidw_interpolate_partial(aidw_t h, const void *qx, const void *qy, i
     CK(h, cudaSetDevice(h->device));
     return launched(h,
                     aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, alpha, 0.0, d1sq, nullptr,
-                                        static_cast<cudaStream_t>(stream), partial_out),
+                                        static_cast<cudaStream_t>(stream), partial_out, perm_for(h, nq),
+                                        h->sc->cls),
                     "interpolate partial kernel");
 }
 
@@ -542,11 +573,12 @@ aidw_status aidw_destroy(aidw_t h)
 {
     if (!h) return AIDW_OK;
     cudaSetDevice(h->device);
-    if (h->data || h->sc || h->work || h->filt.arrays) cudaDeviceSynchronize();
+    if (h->data || h->sc || h->work || h->filt.arrays || h->perm) cudaDeviceSynchronize();
     if (h->data) cudaFree(h->data);
     if (h->sc) cudaFree(h->sc);
     if (h->work) cudaFree(h->work);
     if (h->filt.arrays) cudaFree(h->filt.arrays);
+    if (h->perm) cudaFree(h->perm);
     delete h;
     return AIDW_OK;
 }

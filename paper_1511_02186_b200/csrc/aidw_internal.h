@@ -27,6 +27,7 @@ struct Scratch {
     long long err_idx;          // smallest non-finite query index (LLONG_MAX = none)
     unsigned long long keys[4]; // bbox: ordered keys of min x, max x, min y, max y
     unsigned long long nonfinite;
+    unsigned cls[8];            // weighting-pass class counts + cursors (launch_interp)
 };
 
 // fp32 kNN filter data owned by a handle: centred coordinates and
@@ -70,8 +71,12 @@ int launch_paper(int variant, int dtype, int layout, const void *data, int64_t n
 // alpha == nullptr -> every query uses alpha_const (standard IDW, Eq. 1 with a constant power).
 // partial != nullptr -> write per-query fp64 {sum w, sum w z, sum z_coincident, n_coincident}
 // over this handle's data (data-sharded mode) instead of z.
+// perm (int32[nq]) + cls_counts (uint32[8]) != nullptr -> fp32: queries are grouped by
+// exact-exponent class first (2 small kernels) so whole CTAs take the 1-SFU-op paths.
+// Returns the number of kernels launched.
 int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const void *qx,
                   const void *qy, int64_t nq, const void *alpha, double alpha_const, const void *d1sq, void *z,
-                  cudaStream_t st, double *partial = nullptr);
+                  cudaStream_t st, double *partial = nullptr, int *perm = nullptr,
+                  unsigned *cls_counts = nullptr);
 
 }  // namespace aidw

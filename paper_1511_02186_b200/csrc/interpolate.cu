@@ -27,6 +27,7 @@ template <typename T> struct InterpArgs {
     T *z;
     T alpha_const;
     double *partial;  // nullable: data-sharded partial sums instead of z
+    const int *perm;  // nullable: position i evaluates query perm[i] (class grouping)
 };
 
 __device__ __forceinline__ float wlog2(float s) { return lg2_approx(s); }
@@ -127,9 +128,11 @@ __global__ void __launch_bounds__(kBlock) interp_kernel(const InterpArgs<T> a)
                             a.pz, a.nd);
 }
 
-// Packed fp32 kernel (passes.cuh interp_f32_tile).
+// Packed fp32 kernel (passes.cuh interp_f32_tile / interp_f32_tile_cls).  With a class
+// permutation, a CTA whose queries all share an exact-exponent class runs the 1-SFU-op
+// loop; a CTA mixing classes (only at class boundaries) selects per lane.
 template <int Q, unsigned EMU>
-__global__ void __launch_bounds__(kBlock) interp_f32x2_kernel(const InterpArgs<float> a)
+__global__ void __launch_bounds__(kBlock, 9) interp_f32x2_kernel(const InterpArgs<float> a)
 {
     constexpr int TILE = kTileW, STAGES = kStagesW;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -143,30 +146,93 @@ __global__ void __launch_bounds__(kBlock) interp_f32x2_kernel(const InterpArgs<f
 
     const int64_t base = (int64_t)blockIdx.x * (kBlock * Q) + threadIdx.x;
     float qx[Q], qy[Q], d1[Q];
+    int64_t qid[Q];
+    int cls[Q];
     bool valid[Q];
+    unsigned present = 0;
     InterpF32State<Q> st;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        const int64_t idx = base + q * kBlock;
-        valid[q] = idx < a.nq;
-        qx[q] = valid[q] ? a.qx[idx] : 0.f;
-        qy[q] = valid[q] ? a.qy[idx] : 0.f;
-        d1[q] = valid[q] ? a.d1sq[idx] : 1.f;
-        st.init(q, qx[q], qy[q], valid[q] ? (a.alpha ? a.alpha[idx] : a.alpha_const) : 1.f, d1[q]);
+        const int64_t i = base + q * kBlock;
+        valid[q] = i < a.nq;
+        qid[q] = valid[q] ? (a.perm ? (int64_t)a.perm[i] : i) : 0;
+        qx[q] = valid[q] ? a.qx[qid[q]] : 0.f;
+        qy[q] = valid[q] ? a.qy[qid[q]] : 0.f;
+        d1[q] = valid[q] ? a.d1sq[qid[q]] : 1.f;
+        const float al = valid[q] ? (a.alpha ? a.alpha[qid[q]] : a.alpha_const) : 1.f;
+        st.init(q, qx[q], qy[q], al, d1[q]);
+        cls[q] = a.perm ? alpha_class(al, d1[q]) : kClsGeneral;
+        if (valid[q]) present |= 1u << cls[q];
+    }
+    int cta_cls = kClsGeneral;
+    if (a.perm) {
+        const int any_g = __syncthreads_or(present & 1u), any_1 = __syncthreads_or(present & 2u);
+        const int any_2 = __syncthreads_or(present & 4u), any_3 = __syncthreads_or(present & 8u);
+        const int n = (any_g != 0) + (any_1 != 0) + (any_2 != 0) + (any_3 != 0);
+        cta_cls = n > 1 ? kClsMixed : any_1 ? kClsA1 : any_2 ? kClsA2 : any_3 ? kClsA3 : kClsGeneral;
     }
 
     for (int t = 0; t < ntiles; ++t) {
         r.ring.wait_full(t);
         const int o = r.ring.slot(t) * TILE;
-        interp_f32_tile<Q, EMU, TILE>(st, r.sx + o, r.sy + o, r.sz + o);
+        switch (cta_cls) {  // CTA-uniform
+        case kClsA1: interp_f32_tile_cls<Q, kClsA1, EMU, TILE>(st, cls, r.sx + o, r.sy + o, r.sz + o); break;
+        case kClsA2: interp_f32_tile_cls<Q, kClsA2, EMU, TILE>(st, cls, r.sx + o, r.sy + o, r.sz + o); break;
+        case kClsA3: interp_f32_tile_cls<Q, kClsA3, EMU, TILE>(st, cls, r.sx + o, r.sy + o, r.sz + o); break;
+        case kClsMixed: interp_f32_tile_cls<Q, kClsMixed, EMU, TILE>(st, cls, r.sx + o, r.sy + o, r.sz + o); break;
+        default: interp_f32_tile<Q, EMU, TILE>(st, r.sx + o, r.sy + o, r.sz + o); break;
+        }
         r.ring.release(t, ntiles, issue);
     }
 
 #pragma unroll
     for (int q = 0; q < Q; ++q)
         if (valid[q])
-            write_result<float>(a.z, a.partial, base + q * kBlock, st.SW[q], st.SWZ[q], d1[q], qx[q], qy[q], a.px,
-                                a.py, a.pz, a.nd);
+            write_result<float>(a.z, a.partial, qid[q], st.SW[q], st.SWZ[q], d1[q], qx[q], qy[q], a.px, a.py, a.pz,
+                                a.nd);
+}
+
+// Class grouping (2 small kernels): counts per class, then a scatter into perm in the
+// order alpha = 3, 2, 1, general: the class boundaries -- the only CTAs that mix classes
+// and run slower -- fall in the first CTAs, never in the tail of the launch.
+__device__ __forceinline__ int class_of(const InterpArgs<float> &a, int64_t i)
+{
+    return alpha_class(a.alpha ? a.alpha[i] : a.alpha_const, a.d1sq[i]);
+}
+
+__global__ void class_count_kernel(const InterpArgs<float> a, unsigned *counts)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < a.nq; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        const int c = i < a.nq ? class_of(a, i) : -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const unsigned m = __ballot_sync(0xffffffffu, c == k);
+            if (lane == 0 && m) atomicAdd(&counts[k], __popc(m));
+        }
+    }
+}
+
+__global__ void class_scatter_kernel(const InterpArgs<float> a, unsigned *counts, int *perm)
+{
+    const int lane = threadIdx.x & 31;
+    // offsets for classes 0 (general), 1, 2, 3 with the order 3, 2, 1, 0 in perm
+    const unsigned off[4] = {counts[3] + counts[2] + counts[1], counts[3] + counts[2], counts[3], 0u};
+    unsigned *cursor = counts + 4;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < a.nq; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        const int c = i < a.nq ? class_of(a, i) : -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const unsigned m = __ballot_sync(0xffffffffu, c == k);
+            if (!m) continue;
+            unsigned b = 0;
+            if (lane == 0) b = atomicAdd(&cursor[k], __popc(m));
+            b = __shfl_sync(0xffffffffu, b, 0);
+            if (c == k) perm[off[k] + b + __popc(m & ((1u << lane) - 1u))] = (int)i;
+        }
+    }
 }
 
 template <typename T, int Q>
@@ -252,18 +318,31 @@ int launch_finalize(int dtype, const double *partials, int P, int64_t nq, void *
 
 int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const void *qx,
                   const void *qy, int64_t nq, const void *alpha, double alpha_const, const void *d1sq, void *z,
-                  cudaStream_t st, double *partial)
+                  cudaStream_t st, double *partial, int *perm, unsigned *cls_counts)
 {
     if (dtype == 0) {
         const float *p = static_cast<const float *>(data);
         InterpArgs<float> a{p, p + ndp, p + 2 * ndp, ndp, nd, (const float *)qx, (const float *)qy,
                             (const float *)alpha, (const float *)d1sq, nq, (float *)z, (float)alpha_const,
-                            partial};
-        return launch_interp_f32(a, st);
+                            partial, nullptr};
+        int launches = 0;
+        if (perm && cls_counts && interp_variant() != 1) {
+            if (cudaMemsetAsync(cls_counts, 0, 8 * sizeof(unsigned), st) != cudaSuccess) return -1;
+            int64_t blocks = (nq + 255) / 256;
+            if (blocks > 148 * 8) blocks = 148 * 8;
+            class_count_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, cls_counts);
+            class_scatter_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, cls_counts, perm);
+            if (cudaPeekAtLastError() != cudaSuccess) return -1;
+            launches = 2;
+            a.perm = perm;
+        }
+        const int n = launch_interp_f32(a, st);
+        return n < 0 ? -1 : n + launches;
     }
     const double *p = static_cast<const double *>(data);
     InterpArgs<double> a{p, p + ndp, p + 2 * ndp, ndp, nd, (const double *)qx, (const double *)qy,
-                         (const double *)alpha, (const double *)d1sq, nq, (double *)z, alpha_const, partial};
+                         (const double *)alpha, (const double *)d1sq, nq, (double *)z, alpha_const, partial,
+                         nullptr};
     return launch_interp_t<double, 2>(a, st);
 }
 

@@ -316,6 +316,105 @@ __device__ __forceinline__ void interp_f32_tile(InterpF32State<Q> &st, const flo
     }
 }
 
+// ---------------------------------------------------------------------------------
+// Exact-exponent classes of the weighting pass: Eq. 6 is flat on
+// mu <= 0.1 (alpha = alpha_1) and mu >= 0.9 (alpha = alpha_5), so whole ranges of queries
+// share one power; when that power is 1, 2 or 3 the weight d^-alpha needs ONE SFU op
+// instead of log2 + exp2:  alpha = 1: w = rsqrt(s);  2: w = rcp(s);  3: w = rsqrt(s)^3.
+// (Unscaled by the nearest distance -- the factor cancels in Eq. 1 and these powers
+// cannot overflow fp32 for distances >= 2^-42.)  A query's class depends only on its
+// alpha VALUE, so its arithmetic never depends on which CTA or slot evaluates it.
+enum : int { kClsGeneral = 0, kClsA1 = 1, kClsA2 = 2, kClsA3 = 3, kClsMixed = 4 };
+
+// The unscaled special weights stay in fp32 range (no overflow of a 512-term tile sum,
+// no underflow of the nearest weights) for 2^-78 <= d1sq <= 2^66; outside it the
+// general, nearest-scaled formula is used.
+__device__ __forceinline__ int alpha_class(float alpha, float d1sq)
+{
+    if (!(d1sq >= 0x1p-78f && d1sq <= 0x1p66f)) return kClsGeneral;
+    return alpha == 1.0f ? kClsA1 : alpha == 2.0f ? kClsA2 : alpha == 3.0f ? kClsA3 : kClsGeneral;
+}
+
+template <int CLS>
+__device__ __forceinline__ f32x2 special_w(f32x2 s)
+{
+    if (CLS == kClsA1) return pack2(rsqrt_approx(s.x), rsqrt_approx(s.y));
+    if (CLS == kClsA2) return pack2(rcp_approx(s.x), rcp_approx(s.y));
+    const f32x2 r = pack2(rsqrt_approx(s.x), rsqrt_approx(s.y));
+    return mul2(mul2(r, r), r);
+}
+
+// One 4-point group for a CTA whose queries all have class CLS (A1/A2/A3), or, for
+// CLS == kClsMixed, per-lane selection among the four formulas (rare: class boundaries).
+template <int Q, int CLS, unsigned HMASK>
+__device__ __forceinline__ void interp_f32_group_cls(InterpF32State<Q> &st, const int (&cls)[Q],
+                                                     f32x2 (&sw)[Q], f32x2 (&swz)[Q], const float *__restrict__ tx,
+                                                     const float *__restrict__ ty, const float *__restrict__ tz)
+{
+    const float4 X = *reinterpret_cast<const float4 *>(tx);
+    const float4 Y = *reinterpret_cast<const float4 *>(ty);
+    const float4 Z = *reinterpret_cast<const float4 *>(tz);
+    const f32x2 Xh[2] = {pack2(X.x, X.y), pack2(X.z, X.w)};
+    const f32x2 Yh[2] = {pack2(Y.x, Y.y), pack2(Y.z, Y.w)};
+    const f32x2 Zh[2] = {pack2(Z.x, Z.y), pack2(Z.z, Z.w)};
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const f32x2 dx = sub2(st.QX[q], Xh[h]);
+            const f32x2 dy = sub2(st.QY[q], Yh[h]);
+            const f32x2 s = fma2(dx, dx, mul2(dy, dy));
+            f32x2 w;
+            if (CLS != kClsMixed) {
+                w = special_w<CLS>(s);
+            } else {
+                const int c = cls[q];
+                if (c == kClsA1)
+                    w = special_w<kClsA1>(s);
+                else if (c == kClsA2)
+                    w = special_w<kClsA2>(s);
+                else if (c == kClsA3)
+                    w = special_w<kClsA3>(s);
+                else {  // the general formula with the SAME offload choice as interp_f32_group
+                    const f32x2 l = pack2(lg2_approx(s.x), lg2_approx(s.y));
+                    const f32x2 e = fma2(st.C[q], l, st.B[q]);
+                    const unsigned m = (HMASK >> (2 * h)) & 3u;
+                    if (m == 1u)
+                        w = exp2_poly2(e);
+                    else if (m == 2u)
+                        w = pack2(ex2_approx(e.x), exp2_poly1(e.y));
+                    else
+                        w = pack2(ex2_approx(e.x), ex2_approx(e.y));
+                }
+            }
+            sw[q] = add2(sw[q], w);
+            swz[q] = fma2(w, Zh[h], swz[q]);
+        }
+}
+
+template <int Q, int CLS, unsigned EMU, int TILE>
+__device__ __forceinline__ void interp_f32_tile_cls(InterpF32State<Q> &st, const int (&cls)[Q],
+                                                    const float *__restrict__ tx, const float *__restrict__ ty,
+                                                    const float *__restrict__ tz)
+{
+    static_assert(TILE % 16 == 0, "tile");
+    f32x2 sw[Q], swz[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) sw[q] = swz[q] = make_float2(0.f, 0.f);
+#pragma unroll 1
+    for (int j = 0; j < TILE; j += 16) {
+        interp_f32_group_cls<Q, CLS, (EMU >> 0) & 15u>(st, cls, sw, swz, tx + j, ty + j, tz + j);
+        interp_f32_group_cls<Q, CLS, (EMU >> 4) & 15u>(st, cls, sw, swz, tx + j + 4, ty + j + 4, tz + j + 4);
+        interp_f32_group_cls<Q, CLS, (EMU >> 8) & 15u>(st, cls, sw, swz, tx + j + 8, ty + j + 8, tz + j + 8);
+        interp_f32_group_cls<Q, CLS, (EMU >> 12) & 15u>(st, cls, sw, swz, tx + j + 12, ty + j + 12, tz + j + 12);
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        st.SW[q] += (double)sw[q].x + (double)sw[q].y;
+        st.SWZ[q] += (double)swz[q].x + (double)swz[q].y;
+    }
+}
+
 // Exact coincidence (R19): the limit of Eq. 1 is the mean z of the data points at
 // distance 0.  Rare; one extra pass over global memory for the calling lane.
 template <typename T>

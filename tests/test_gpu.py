@@ -216,6 +216,20 @@ def test_layouts_identical(P):
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
 
 
+def test_exact_exponent_classes(P, orc):
+    """Queries whose alpha is exactly 1, 2 or 3 (Eq. 6's flat ends) take 1-SFU-op paths;
+    grouping them changes no result beyond tolerance and keeps results independent of
+    the grouping (disabled vs enabled within 1e-5; both within 1e-4 of the oracle)."""
+    x, y, z, qx, qy = datagen.random_cloud(91, 12000, 3001)
+    for lv in ([1, 1.5, 2, 2.5, 3], [2.0, 2.1, 2.2, 2.5, 3.0], [3.0] * 5, [1.0, 1.0, 2.0, 3.0, 3.0]):
+        eng = P.AIDW(x, y, z)
+        zg = eng.run(qx, qy, 10, lv, P.GLOBAL).cpu().numpy()
+        zf = eng.run(qx, qy, 10, lv, P.FIXED, 0.0, 2.0).cpu().numpy()
+        for mode, zz in (("global", zg), ("fixed", zf)):
+            Zo = orc.aidw(x, y, z, qx, qy, 10, lv, mode=mode)
+            assert rel_err(zz, Zo).max() <= 1e-4, (lv, mode)
+
+
 def test_constant_levels_is_idw_and_convex(P, orc):
     x, y, z, qx, qy = datagen.random_cloud(17, 20000, 2000)
     eng = P.AIDW(x, y, z)
@@ -292,7 +306,12 @@ def test_launch_count(P):
     eng = P.AIDW(x, y, z)
     n0 = eng.launches
     eng.run(qx, qy, 10)
-    assert eng.launches - n0 == 3  # knn_robs, alpha, interpolate
+    # knn_robs, alpha, class count + scatter (exact-exponent grouping), interpolate
+    assert eng.launches - n0 == 5
+    e64 = P.AIDW(x, y, z, dtype=torch.float64)
+    n0 = e64.launches
+    e64.run(qx, qy, 10)
+    assert e64.launches - n0 == 3
 
 
 # ------------------------------------------------------------------ N1 / N2
@@ -308,7 +327,10 @@ def test_run_fixed_fused(P, orc, dtype, k):
     assert eng.launches - n0 == (1 if dtype == torch.float32 else 3)
     z3, t3 = eng.run(qx, qy, k, LV, P.FIXED, 0.0, 2.0, trace=True)
     assert torch.equal(tf["r_obs"], t3["r_obs"]) and torch.equal(tf["alpha"], t3["alpha"])
-    assert torch.equal(zf, z3)
+    if dtype == torch.float64:
+        assert torch.equal(zf, z3)
+    else:  # the 3-kernel path evaluates alpha in {1, 2, 3} with rsqrt/rcp (exact-exponent classes)
+        assert rel_err(zf.cpu().numpy(), z3.cpu().numpy().astype(np.float64)).max() <= 2e-5
     Zo = orc.aidw(x, y, z, qx, qy, k, LV, mode="fixed")
     assert rel_err(zf.cpu().numpy(), Zo).max() <= TOL[dtype]
     # a different FIXED window and the printed mu form
@@ -329,7 +351,7 @@ def test_run_fixed_coincident_and_errors(P, orc):
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
-@pytest.mark.parametrize("alpha", [1.0, 2.0, 2.7])
+@pytest.mark.parametrize("alpha", [1.0, 2.0, 2.7, 3.0])
 def test_idw(P, orc, dtype, alpha):
     """N2: standard IDW (constant power) against the oracle's Eq. 1."""
     x, y, z, qx, qy = datagen.random_cloud(60, 9000, 777)

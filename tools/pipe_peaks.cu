@@ -10,6 +10,8 @@ constexpr int kChains = 8;
 
 __device__ __forceinline__ float ex2(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 __device__ __forceinline__ float lg2(float x) { float y; asm volatile("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float rsq(float x) { float y; asm volatile("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float rcp(float x) { float y; asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 
 struct Clk { unsigned long long c0, c1, t0, t1; };
 
@@ -28,6 +30,8 @@ __global__ void bench(float *out, Clk *clk, float seed)
             if (MODE == 0) v[i] = ex2(v[i]);                 // MUFU.EX2
             else if (MODE == 1) v[i] = lg2(v[i]);            // MUFU.LG2
             else if (MODE == 2) v[i] = fmaf(v[i], 1.0000001f, 1e-7f);  // FFMA
+            else if (MODE == 5) v[i] = rsq(v[i]);                          // MUFU.RSQ
+            else if (MODE == 6) v[i] = rcp(v[i]);                          // MUFU.RCP
             else if (MODE == 3) {                                          // FFMA2 (2 FMAs / instr)
                 if (i % 2 == 0) {
                     float2 a = make_float2(v[i], v[i + 1]);
@@ -76,6 +80,9 @@ int main()
     double m3, m4;
     double ex = run<0>(sms, out, clk, &m0), lg = run<1>(sms, out, clk, &m1), fm = run<2>(sms, out, clk, &m2);
     double f2 = run<3>(sms, out, clk, &m3), mix = run<4>(sms, out, clk, &m4);
+    double m5, m6;
+    double rs = run<5>(sms, out, clk, &m5), rc = run<6>(sms, out, clk, &m6);
+    printf("{\"mufu_rsq_per_clk_sm\": %.2f, \"mufu_rcp_per_clk_sm\": %.2f}\n", rs, rc);
     // modes 3/4 count values updated: mode 3 = FMAs (2 per FFMA2 instruction), mode 4 = 1 ex2 + 7 FFMA
     printf("{\"sms\": %d, \"mufu_ex2_per_clk_sm\": %.2f, \"mufu_lg2_per_clk_sm\": %.2f, \"ffma_per_clk_sm\": %.2f, "
            "\"ffma2_fma_per_clk_sm\": %.2f, \"ffma2_instr_per_clk_sm\": %.2f, \"mix_1ex2_7ffma_ops_per_clk_sm\": %.2f, "
