@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 7 python tools/sanitize.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "$tool rc=$?"; tail -3 gpurun_out/sanitize_$tool.log
+done
