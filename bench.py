@@ -185,7 +185,8 @@ def run_reference(args):
 
 
 def workload_name(n, nq=NQ_PER_GPU, mode="global"):
-    rb = "GLOBAL R bounds" if mode == "global" else "FIXED R bounds (0, 2), fused kernel"
+    rb = {"global": "GLOBAL R bounds", "fixed": "FIXED R bounds (0, 2), fused kernel",
+          "fixed3": "FIXED R bounds (0, 2), stage kernels"}[mode]
     if n == 1:
         tag = "C4" if nq == NQ_PER_GPU else "C4-shaped"
         return f"{tag}: 1,024,000 data x {nq:,} queries, k=10, fp32, uniform, {rb}"
@@ -204,9 +205,9 @@ def main():
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no baselines, no flush)")
     ap.add_argument("--nq", type=int, default=NQ_PER_GPU, help="queries per GPU (default C4)")
     ap.add_argument("--ref-queries-per-step", type=int, default=0)
-    ap.add_argument("--mode", default="global", choices=["global", "fixed"],
+    ap.add_argument("--mode", default="global", choices=["global", "fixed", "fixed3"],
                     help="global: 3 kernels + allreduce (north star, default); fixed: R bounds (0, 2), "
-                         "one fused kernel per step (N1)")
+                         "one fused kernel per step (N1); fixed3: R bounds (0, 2) on the stage kernels")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -263,10 +264,13 @@ def main():
         if ev: ev[0].record(st)
         P.aidw_knn_robs(eng.h, qx, qy, K_NN, r_obs, d1, mm, None, st)
         if ev: ev[1].record(st)
-        if group is not None:
+        if group is not None and args.mode == "global":
             allreduce_bounds(mm, group)
         if ev: ev[2].record(st)
-        P.aidw_alpha(eng.h, r_obs, lv, P.GLOBAL, 0.0, 0.0, mm, P.NORMALIZED, al, st)
+        if args.mode == "fixed3":
+            P.aidw_alpha(eng.h, r_obs, lv, P.FIXED, 0.0, 2.0, mm, P.NORMALIZED, al, st)
+        else:
+            P.aidw_alpha(eng.h, r_obs, lv, P.GLOBAL, 0.0, 0.0, mm, P.NORMALIZED, al, st)
         if ev: ev[3].record(st)
         P.aidw_interpolate(eng.h, qx, qy, al, d1, zo, st)
         if ev: ev[4].record(st)
@@ -322,7 +326,12 @@ def main():
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            if args.mode == "fixed":
+            if args.mode == "fixed3":
+                dx = hx.to(dev, non_blocking=True)
+                dy = hy.to(dev, non_blocking=True)
+                zz = eng.run(dx, dy, K_NN, lv, P.FIXED, 0.0, 2.0)
+                hz.copy_(zz, non_blocking=True)
+            elif args.mode == "fixed":
                 dx = hx.to(dev, non_blocking=True)
                 dy = hy.to(dev, non_blocking=True)
                 zz = eng.run_fixed(dx, dy, K_NN, lv, 0.0, 2.0)
@@ -345,6 +354,7 @@ def main():
         e2e = {"value": nq * world / (e2e_ms / 1e3), "unit": "points/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": 2 * 4 * nq * world, "d2h_bytes_per_step": 4 * nq * world,
                "api": ("aidw_run_fixed + torch H2D/D2H (pinned)" if args.mode == "fixed" else
+                       "AIDW.run(FIXED) + torch H2D/D2H (pinned)" if args.mode == "fixed3" else
                        "aidw_run_host (C ABI, pinned host buffers)" if group is None else
                        "AIDW.run + torch H2D/D2H (pinned), allreduce")}
 
@@ -403,7 +413,8 @@ def main():
         "data": "synthetic",
         "config": {"workload": workload_name(world, nq, args.mode), "nd": ND, "nq_per_gpu": nq, "nq_total": nq * world,
                    "k": K_NN, "alpha_levels": list(lv),
-                   "rbounds": "global" if args.mode == "global" else "fixed (0, 2), fused single kernel",
+                   "rbounds": {"global": "global", "fixed": "fixed (0, 2), fused single kernel",
+                               "fixed3": "fixed (0, 2), stage kernels"}[args.mode],
                    "mu": "normalized",
                    "l2": "flushed between steps (256 MiB write outside the timed events)",
                    "parallelism": f"query-sharded x{world}, data replicated"},

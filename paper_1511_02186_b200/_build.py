@@ -10,7 +10,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libaidw.so")
 SOURCES = ["aidw_api.cu", "knn_robs.cu", "interpolate.cu", "alpha_prep.cu", "fused.cu", "paper_kernels.cu"]
-HEADERS = ["aidw_internal.h", "device.cuh", "packed.cuh", "passes.cuh"]
+HEADERS = ["aidw_internal.h", "device.cuh", "packed.cuh", "passes.cuh", "f64_tables.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

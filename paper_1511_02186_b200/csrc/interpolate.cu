@@ -30,10 +30,16 @@ template <typename T> struct InterpArgs {
     const int *perm;  // nullable: position i evaluates query perm[i] (class grouping)
 };
 
-__device__ __forceinline__ float wlog2(float s) { return lg2_approx(s); }
-__device__ __forceinline__ double wlog2(double s) { return log2(s); }
-__device__ __forceinline__ float wexp2(float x) { return ex2_approx(x); }
-__device__ __forceinline__ double wexp2(double x) { return exp2(x); }
+// Weight math per precision: fp32 MUFU (scalar variant), fp64 table + polynomial
+// (passes.cuh log2_f64 / exp2_f64; tables staged in shared memory).
+struct F64Tabs {
+    double2 lg[64];
+    double ex[16];
+};
+__device__ __forceinline__ float wlog2(float s, const F64Tabs &) { return lg2_approx(s); }
+__device__ __forceinline__ double wlog2(double s, const F64Tabs &t) { return log2_f64(s, t.lg); }
+__device__ __forceinline__ float wexp2(float x, const F64Tabs &) { return ex2_approx(x); }
+__device__ __forceinline__ double wexp2(double x, const F64Tabs &t) { return exp2_f64(x, t.ex); }
 __device__ __forceinline__ float log2_q(float s) { return lg2_approx_noftz(s); }
 __device__ __forceinline__ double log2_q(double s) { return log2(s); }
 
@@ -67,9 +73,14 @@ __global__ void __launch_bounds__(kBlock) interp_kernel(const InterpArgs<T> a)
 {
     constexpr int TILE = kTileW, STAGES = kStagesW;
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ F64Tabs tabs;
     XYZRing<T, TILE, STAGES> r(smem_raw);
     const int ntiles = (int)(a.ndp / TILE);
     if (threadIdx.x == 0) r.ring.init();
+    if (sizeof(T) == 8) {
+        if (threadIdx.x < 64) tabs.lg[threadIdx.x] = make_double2(kLog2Tab[threadIdx.x][0], kLog2Tab[threadIdx.x][1]);
+        if (threadIdx.x < 16) tabs.ex[threadIdx.x] = kExp2Tab[threadIdx.x];
+    }
     __syncthreads();
     auto issue = [&](int tile, int slot) { r.issue(a, tile, slot); };
     if (threadIdx.x == 0)
@@ -108,7 +119,7 @@ __global__ void __launch_bounds__(kBlock) interp_kernel(const InterpArgs<T> a)
 #pragma unroll
                 for (int q = 0; q < Q; ++q) {
                     const T s = dist_sq(qx[q], qy[q], X.v[e], Y.v[e]);
-                    const T w = wexp2(fma(c[q], wlog2(s), b[q]));
+                    const T w = wexp2(fma(c[q], wlog2(s, tabs), b[q]), tabs);
                     sw[q] += w;
                     swz[q] = fma(w, Z.v[e], swz[q]);
                 }
