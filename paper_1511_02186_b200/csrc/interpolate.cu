@@ -142,10 +142,15 @@ __global__ void __launch_bounds__(kBlock) interp_kernel(const InterpArgs<T> a)
 // Packed fp32 kernel (passes.cuh interp_f32_tile / interp_f32_tile_cls).  With a class
 // permutation, a CTA whose queries all share an exact-exponent class runs the 1-SFU-op
 // loop; a CTA mixing classes (only at class boundaries) selects per lane.
-template <int Q, unsigned EMU>
-__global__ void __launch_bounds__(kBlock, 9) interp_f32x2_kernel(const InterpArgs<float> a)
+// CTAs per SM to target (register cap): 9 at Q = 2 (56 registers, the smem limit too).
+constexpr int interp_min_blocks(int q) { return q == 1 ? 12 : q == 2 ? 9 : 6; }
+// (the generic XYZRing is shared with the fp64 kernel; its stage count is a template
+// parameter so the packed kernel can trade pipeline depth for occupancy)
+
+template <int Q, unsigned EMU, int STAGES = kStagesW>
+__global__ void __launch_bounds__(kBlock, interp_min_blocks(Q)) interp_f32x2_kernel(const InterpArgs<float> a)
 {
-    constexpr int TILE = kTileW, STAGES = kStagesW;
+    constexpr int TILE = kTileW;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     XYZRing<float, TILE, STAGES> r(smem_raw);
     const int ntiles = (int)(a.ndp / TILE);
@@ -259,16 +264,18 @@ static int launch_interp_t(const InterpArgs<T> &a, cudaStream_t st)
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-template <int Q, unsigned EMU>
+template <int Q, unsigned EMU, int STAGES = kStagesW>
 static int launch_interp_f32x2(const InterpArgs<float> &a, cudaStream_t st)
 {
-    const size_t smem = XYZRing<float, kTileW, kStagesW>::smem_bytes();
-    if (cudaFuncSetAttribute(interp_f32x2_kernel<Q, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
+    const size_t smem = XYZRing<float, kTileW, STAGES>::smem_bytes();
+    if (cudaFuncSetAttribute(interp_f32x2_kernel<Q, EMU, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(interp_f32x2_kernel<Q, EMU, STAGES>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             100) != cudaSuccess)
         return -1;
     const int64_t per_cta = (int64_t)kBlock * Q;
     const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
-    interp_f32x2_kernel<Q, EMU><<<grid, kBlock, smem, st>>>(a);
+    interp_f32x2_kernel<Q, EMU, STAGES><<<grid, kBlock, smem, st>>>(a);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -295,7 +302,15 @@ static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st)
     case 6: return launch_interp_f32x2<2, 0x2222>(a, st);   // f = 1/4, split
     case 7: return launch_interp_f32x2<2, 0x22A2>(a, st);   // f = 5/16, split
     case 8: return launch_interp_f32x2<2, 0x1241>(a, st);   // f = 3/8, packed + one split
-    default: return launch_interp_f32x2<2, 0x0141>(a, st); // f = 3/8 packed (best measured, r01)
+    case 9: return launch_interp_f32x2<1, 0x0141>(a, st);   // Q = 1
+    case 10: return launch_interp_f32x2<3, 0x0141>(a, st);  // Q = 3
+    case 11: return launch_interp_f32x2<4, 0x0141>(a, st);  // Q = 4
+    case 12: return launch_interp_f32x2<1, 0x0141, 3>(a, st);  // Q = 1, 3 stages (12 CTAs/SM)
+    case 13: return launch_interp_f32x2<1, 0x0141, 2>(a, st);  // Q = 1, 2 stages
+    case 14: return launch_interp_f32x2<1, 0x1111, 3>(a, st);  // Q = 1, 3 stages, f = 1/2
+    case 15: return launch_interp_f32x2<2, 0x0141, 3>(a, st);  // Q = 2, 3 stages
+    case 16: return launch_interp_f32x2<2, 0x0141>(a, st);  // Q = 2
+    default: return launch_interp_f32x2<1, 0x0141>(a, st); // Q = 1, f = 3/8 packed (best measured, r01)
     }
 }
 
