@@ -166,7 +166,7 @@ __device__ __forceinline__ void knn_f32_tile(KnnF32State<K, Q> &st, const float 
                     tv[q][c + 2 * h + 1] = tt.y;
                 }
         }
-        bool hit = false;
+        bool hq[Q], hit = false;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             float m[G];
@@ -176,14 +176,19 @@ __device__ __forceinline__ void knn_f32_tile(KnnF32State<K, Q> &st, const float 
             for (int w = 1; w < G; w *= 2)
 #pragma unroll
                 for (int i = 0; i + w < G; i += 2 * w) m[i] = fminf(m[i], m[i + w]);
-            hit |= m[0] <= st.thr[q];
+            hq[q] = m[0] <= st.thr[q];
+            hit |= hq[q];
         }
         if (__any_sync(0xffffffffu, hit)) {
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
+                if (!__any_sync(0xffffffffu, hq[q])) continue;
                 unsigned mask = 0;
+                if (hq[q]) {
 #pragma unroll
-                for (int e = 0; e < G; ++e) mask |= (tv[q][e] <= st.thr[q]) ? (1u << e) : 0u;
+                    for (int e = 0; e < G; ++e) mask |= (tv[q][e] <= st.thr[q]) ? (1u << e) : 0u;
+                }
+                bool inserted = false;
                 while (__any_sync(0xffffffffu, mask != 0)) {
                     if (mask) {
                         const int e = __ffs(mask) - 1;
@@ -191,10 +196,13 @@ __device__ __forceinline__ void knn_f32_tile(KnnF32State<K, Q> &st, const float 
                         const float s = dist_sq(st.qx[q], st.qy[q], tpx[j + e], tpy[j + e]);
                         if (s < st.buf[q][K - 1]) {
                             topk_insert<float, K>(st.buf[q], s);
-                            st.thr[q] = thr_of(st.buf[q][K - 1], st.qqf[q], st.mf[q], st.Ef[q]);
+                            inserted = true;
                         }
                     }
                 }
+                // one threshold update per group (candidates of this group were all
+                // checked exactly against the current k-th distance above)
+                if (inserted) st.thr[q] = thr_of(st.buf[q][K - 1], st.qqf[q], st.mf[q], st.Ef[q]);
             }
         }
     }
