@@ -44,10 +44,10 @@ __device__ __forceinline__ float log2_q(float s) { return lg2_approx_noftz(s); }
 __device__ __forceinline__ double log2_q(double s) { return log2(s); }
 
 // Ring + smem tile layout shared by both kernels: x, y, z arrays of STAGES * TILE.
-template <typename T, int TILE, int STAGES>
+template <typename T, int TILE, int STAGES, int WARPS = kWarps>
 struct XYZRing {
     T *sx, *sy, *sz;
-    Ring<STAGES> ring;
+    Ring<STAGES, WARPS> ring;
     __device__ __forceinline__ XYZRing(unsigned char *smem)
     {
         sx = reinterpret_cast<T *>(smem);
@@ -147,12 +147,13 @@ constexpr int interp_min_blocks(int q) { return q == 1 ? 12 : q == 2 ? 9 : 6; }
 // (the generic XYZRing is shared with the fp64 kernel; its stage count is a template
 // parameter so the packed kernel can trade pipeline depth for occupancy)
 
-template <int Q, unsigned EMU, int STAGES = kStagesW>
-__global__ void __launch_bounds__(kBlock, interp_min_blocks(Q)) interp_f32x2_kernel(const InterpArgs<float> a)
+template <int Q, unsigned EMU, int STAGES = kStagesW, int BLOCK = kBlock>
+__global__ void __launch_bounds__(BLOCK, interp_min_blocks(Q) * kBlock / BLOCK)
+    interp_f32x2_kernel(const InterpArgs<float> a)
 {
     constexpr int TILE = kTileW;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    XYZRing<float, TILE, STAGES> r(smem_raw);
+    XYZRing<float, TILE, STAGES, BLOCK / 32> r(smem_raw);
     const int ntiles = (int)(a.ndp / TILE);
     if (threadIdx.x == 0) r.ring.init();
     __syncthreads();
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(kBlock, interp_min_blocks(Q)) interp_f32x2_ker
     if (threadIdx.x == 0)
         for (int s = 0; s < STAGES && s < ntiles; ++s) issue(s, s);
 
-    const int64_t base = (int64_t)blockIdx.x * (kBlock * Q) + threadIdx.x;
+    const int64_t base = (int64_t)blockIdx.x * (BLOCK * Q) + threadIdx.x;
     float qx[Q], qy[Q], d1[Q];
     int64_t qid[Q];
     int cls[Q];
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(kBlock, interp_min_blocks(Q)) interp_f32x2_ker
     InterpF32State<Q> st;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        const int64_t i = base + q * kBlock;
+        const int64_t i = base + q * BLOCK;
         valid[q] = i < a.nq;
         qid[q] = valid[q] ? (a.perm ? (int64_t)a.perm[i] : i) : 0;
         qx[q] = valid[q] ? a.qx[qid[q]] : 0.f;
@@ -264,18 +265,17 @@ static int launch_interp_t(const InterpArgs<T> &a, cudaStream_t st)
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-template <int Q, unsigned EMU, int STAGES = kStagesW>
+template <int Q, unsigned EMU, int STAGES = kStagesW, int BLOCK = kBlock>
 static int launch_interp_f32x2(const InterpArgs<float> &a, cudaStream_t st)
 {
     const size_t smem = XYZRing<float, kTileW, STAGES>::smem_bytes();
-    if (cudaFuncSetAttribute(interp_f32x2_kernel<Q, EMU, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess ||
-        cudaFuncSetAttribute(interp_f32x2_kernel<Q, EMU, STAGES>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             100) != cudaSuccess)
+    auto kern = interp_f32x2_kernel<Q, EMU, STAGES, BLOCK>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
         return -1;
-    const int64_t per_cta = (int64_t)kBlock * Q;
+    const int64_t per_cta = (int64_t)BLOCK * Q;
     const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
-    interp_f32x2_kernel<Q, EMU, STAGES><<<grid, kBlock, smem, st>>>(a);
+    kern<<<grid, BLOCK, smem, st>>>(a);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -310,6 +310,9 @@ static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st)
     case 14: return launch_interp_f32x2<1, 0x1111, 3>(a, st);  // Q = 1, 3 stages, f = 1/2
     case 15: return launch_interp_f32x2<2, 0x0141, 3>(a, st);  // Q = 2, 3 stages
     case 16: return launch_interp_f32x2<2, 0x0141>(a, st);  // Q = 2
+    case 17: return launch_interp_f32x2<1, 0x0141, 4, 256>(a, st);  // Q = 1, 256-thread CTAs
+    case 18: return launch_interp_f32x2<1, 0x0141, 4, 512>(a, st);  // Q = 1, 512-thread CTAs
+    case 19: return launch_interp_f32x2<2, 0x0141, 4, 256>(a, st);  // Q = 2, 256-thread CTAs
     default: return launch_interp_f32x2<1, 0x0141>(a, st); // Q = 1, f = 3/8 packed (best measured, r01)
     }
 }

@@ -14,7 +14,7 @@ namespace aidw {
 // ------------------------------------------------------------------ tile ring
 // STAGES smem slots filled by the TMA engine (one elected producer thread), consumed
 // by all warps.  Tile t lives in slot t % STAGES; full/empty barrier parity (t/S) & 1.
-template <int STAGES>
+template <int STAGES, int WARPS = kWarps>
 struct Ring {
     uint64_t *full, *empty;
 
@@ -22,7 +22,7 @@ struct Ring {
     {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kWarps);
+            mbar_init(&empty[s], WARPS);
         }
         fence_mbar_init();
     }
