@@ -259,12 +259,21 @@ class AIDW:
         """Whole path for this rank's queries; GLOBAL bounds are allreduced over
         ``group`` (torch.distributed) when given."""
         from .partition import allreduce_bounds
+        nvtx = torch.cuda.nvtx
         qx, qy = self._q(qx), self._q(qy)
+        nvtx.range_push("aidw.knn_robs")  # NVTX ranges for Nsight timelines (SURVEY §5 tracing)
         r_obs, d1sq, mm = self.knn_robs(qx, qy, k, stream=stream)
+        nvtx.range_pop()
         if rbounds == GLOBAL and group is not None:
+            nvtx.range_push("aidw.allreduce_bounds")
             allreduce_bounds(mm, group)
+            nvtx.range_pop()
+        nvtx.range_push("aidw.alpha")
         a = self.alpha(r_obs, levels, rbounds, r_min, r_max, mm, muform, stream)
+        nvtx.range_pop()
+        nvtx.range_push("aidw.interpolate")
         z = self.interpolate(qx, qy, a, d1sq, stream)
+        nvtx.range_pop()
         if trace:
             return z, dict(r_obs=r_obs, d1sq=d1sq, minmax=mm, alpha=a)
         return z
