@@ -439,3 +439,20 @@ def test_C5_grid_full_size_sampled(P, orc):
     a_o = orc.alpha(ro64, re, LV, -float(mmc[0]) / re, float(mmc[1]) / re)
     Zo = orc.idw(x, y, z, qx[sub], qy[sub], a_o)
     assert rel_err(zg[sub], Zo).max() <= 1e-4
+
+
+@pytest.mark.parametrize("offset,scale", [(0.0, 2.0 ** -30), (1000.0, 1.0), (-3.0e4, 16.0), (0.5, 2.0 ** 20)])
+def test_knn_filter_translated_scaled(P, orc, offset, scale):
+    """The fp32 kNN filter's rounding margin holds for coordinates far from the origin
+    and at extreme scales: selection stays bit-exact against the oracle's float
+    instantiation (same fp32 inputs), Z within tolerance of the fp64 oracle."""
+    x, y, z, qx, qy = datagen.random_cloud(303, 6000, 900)
+    f = lambda v: (offset + scale * v).astype(np.float32).astype(np.float64)
+    x, y, qx, qy = f(x), f(y), f(qx), f(qy)
+    eng = P.AIDW(x, y, z)
+    r, d1, mm, d = gpu_knn(P, eng, qx, qy, 10)
+    ro, do = orc.knn_f32(x, y, qx, qy, 10, want_dists=True)
+    assert np.array_equal(d, do) and np.array_equal(r, ro)
+    Zg = eng.run(qx, qy, 10, LV, P.GLOBAL).cpu().numpy()
+    Zo = orc.aidw(x, y, z, qx, qy, 10, LV, mode="global")
+    assert rel_err(Zg, Zo).max() <= 1e-4
