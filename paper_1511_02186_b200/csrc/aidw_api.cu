@@ -23,10 +23,30 @@ struct aidw_ctx {
     size_t work_bytes = 0;
     int *perm = nullptr;             // weighting-pass class permutation (fp32)
     int64_t perm_cap = 0;
+    aidw::SplitBuf split;            // small-nq data split scratch
     int64_t launches = 0;
     double bbox[4] = {0, 0, 0, 0};
     char err[512] = {0};
 };
+
+void *aidw::SplitBuf::reserve(size_t n)
+{
+    if (n <= bytes) return p;
+    if (p) {
+        cudaDeviceSynchronize();
+        cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    n = (n + (size_t(1) << 20) - 1) >> 20 << 20;
+    if (cudaMalloc(&p, n) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        return nullptr;
+    }
+    bytes = n;
+    return p;
+}
 
 namespace {
 
@@ -108,6 +128,14 @@ int *perm_for(aidw_t h, int64_t nq)
         h->perm_cap = nq;
     }
     return h->perm;
+}
+
+// Small-nq data split: the handle's growable scratch, or nullptr when
+// nq is large enough that the query grid alone fills the GPU.
+aidw::SplitBuf *split_for(aidw_t h, int64_t nq)
+{
+    constexpr int64_t kSplitMaxQ = int64_t(1) << 20;
+    return nq <= kSplitMaxQ ? &h->split : nullptr;
 }
 
 bool is_device_ptr(const void *p)
@@ -305,7 +333,7 @@ aidw_status aidw_knn_robs(aidw_t h, const void *qx, const void *qy, int64_t nq, 
     }
     return launched(h,
                     aidw::launch_knn((int)h->dt, k, h->data, h->ndp, qx, qy, nq, r_obs, d1sq, robs_minmax,
-                                     knn_dists, h->sc, &h->filt, st),
+                                     knn_dists, h->sc, &h->filt, st, 0, split_for(h, nq)),
                     "knn_robs kernel");
 }
 
@@ -352,14 +380,15 @@ aidw_status aidw_interpolate(aidw_t h, const void *qx, const void *qy, int64_t n
         void *d1 = static_cast<char *>(h->work) + ((size_t)nq * ts + 255) / 256 * 256;
         s = launched(h,
                      aidw::launch_knn((int)h->dt, 1, h->data, h->ndp, qx, qy, nq, robs, d1, nullptr, nullptr,
-                                      h->sc, &h->filt, st),
+                                      h->sc, &h->filt, st, 0, split_for(h, nq)),
                      "nearest kernel");
         if (s != AIDW_OK) return s;
         d1sq = d1;
     }
+    aidw::SplitBuf *sp = split_for(h, nq);
     return launched(h,
                     aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, alpha, 0.0, d1sq, z_out, st,
-                                        nullptr, perm_for(h, nq), h->sc->cls),
+                                        nullptr, perm_for(h, nq), h->sc->cls, sp),
                     "interpolate kernel");
 }
 
@@ -415,12 +444,13 @@ aidw_status aidw_idw(aidw_t h, const void *qx, const void *qy, int64_t nq, doubl
     char *w = static_cast<char *>(h->work);
     s = launched(h,
                  aidw::launch_knn((int)h->dt, 1, h->data, h->ndp, qx, qy, nq, w, w + nb, nullptr, nullptr, h->sc,
-                                  &h->filt, st),
+                                  &h->filt, st, 0, split_for(h, nq)),
                  "nearest kernel");
     if (s != AIDW_OK) return s;
+    aidw::SplitBuf *sp = split_for(h, nq);
     return launched(h,
                     aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, nullptr, alpha, w + nb,
-                                        z_out, st, nullptr, perm_for(h, nq), h->sc->cls),
+                                        z_out, st, nullptr, perm_for(h, nq), h->sc->cls, sp),
                     "interpolate kernel");
 }
 
@@ -474,7 +504,7 @@ aidw_status aidw_knn_partial(aidw_t h, const void *qx, const void *qy, int64_t n
     CK(h, cudaSetDevice(h->device));
     return launched(h,
                     aidw::launch_knn((int)h->dt, k, h->data, h->ndp, qx, qy, nq, nullptr, nullptr, nullptr, s_out,
-                                     h->sc, &h->filt, static_cast<cudaStream_t>(stream), 1),
+                                     h->sc, &h->filt, static_cast<cudaStream_t>(stream), 1, split_for(h, nq)),
                     "knn partial kernel");
 }
 
@@ -502,10 +532,11 @@ aidw_status aidw_interpolate_partial(aidw_t h, const void *qx, const void *qy, i
     if (nq == 0) return AIDW_OK;
     if (!qx || !qy || !alpha || !d1sq || !partial_out) return fail(h, AIDW_E_INVALID_ARG, "NULL argument");
     CK(h, cudaSetDevice(h->device));
+    aidw::SplitBuf *sp = split_for(h, nq);
     return launched(h,
                     aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, alpha, 0.0, d1sq, nullptr,
                                         static_cast<cudaStream_t>(stream), partial_out, perm_for(h, nq),
-                                        h->sc->cls),
+                                        h->sc->cls, sp),
                     "interpolate partial kernel");
 }
 
@@ -573,12 +604,13 @@ aidw_status aidw_destroy(aidw_t h)
 {
     if (!h) return AIDW_OK;
     cudaSetDevice(h->device);
-    if (h->data || h->sc || h->work || h->filt.arrays || h->perm) cudaDeviceSynchronize();
+    if (h->data || h->sc || h->work || h->filt.arrays || h->perm || h->split.p) cudaDeviceSynchronize();
     if (h->data) cudaFree(h->data);
     if (h->sc) cudaFree(h->sc);
     if (h->work) cudaFree(h->work);
     if (h->filt.arrays) cudaFree(h->filt.arrays);
     if (h->perm) cudaFree(h->perm);
+    if (h->split.p) cudaFree(h->split.p);
     delete h;
     return AIDW_OK;
 }

@@ -18,6 +18,27 @@ constexpr int kTileKF = 512;   // points per smem stage, fp32 filtered kNN (cx, 
 constexpr int kStagesKF = 3;
 constexpr int kPad = 1024;     // internal arrays padded to a multiple of both tiles
 
+// The fp64 cross-tile sums of the weighting pass are formed per accumulation block of
+// tiles (at most kAccBlocks per data set, boundaries depending only on nd) and the
+// block sums are added in block order.  A launch that splits the data range across
+// CTAs (small nq, "split mode") writes per-block sums and adds them in the same order
+// afterwards, so split and unsplit launches give bit-identical Z.
+constexpr int kAccBlocks = 16;
+__host__ __device__ inline int acc_blocks(int ntiles) { return ntiles < kAccBlocks ? ntiles : kAccBlocks; }
+__host__ __device__ inline int block_tile(int b, int ntiles, int nblk)
+{
+    return (int)((long long)b * ntiles / nblk);
+}
+
+// Growable device buffer for the small-nq data split (per-split kNN lists, per-block
+// weighting sums).  reserve() grows it (device sync + free + malloc) and returns
+// nullptr on allocation failure, in which case the launcher runs unsplit.
+struct SplitBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    void *reserve(size_t n);
+};
+
 // Device scratch owned by a handle.
 struct Scratch {
     unsigned long long mn;      // ordered bits of min r_obs (identity ~0ull)
@@ -44,7 +65,7 @@ int launch_prep(int dtype, int layout, const void *src, int64_t nd, int64_t ndp,
 
 int launch_knn(int dtype, int k, const void *data, int64_t ndp, const void *qx, const void *qy,
                int64_t nq, void *r_obs, void *d1sq, void *minmax, void *dists, Scratch *sc,
-               const FilterData *filt, cudaStream_t st, int dists_sq = 0);
+               const FilterData *filt, cudaStream_t st, int dists_sq = 0, SplitBuf *split = nullptr);
 
 int launch_knn_merge(int dtype, int k, const void *lists, int P, int64_t nq, void *r_obs, void *d1sq,
                      void *minmax, Scratch *sc, cudaStream_t st);
@@ -77,6 +98,10 @@ int launch_paper(int variant, int dtype, int layout, const void *data, int64_t n
 int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const void *qx,
                   const void *qy, int64_t nq, const void *alpha, double alpha_const, const void *d1sq, void *z,
                   cudaStream_t st, double *partial = nullptr, int *perm = nullptr,
-                  unsigned *cls_counts = nullptr);
+                  unsigned *cls_counts = nullptr, SplitBuf *split = nullptr);
+
+// Data-split factor for a launch of `grid` CTAs (small nq fills the GPU by splitting the
+// data range across blockIdx.y); 1 = no split.
+int choose_split(const void *kern, int block, size_t smem, int64_t grid, int maxs, int waves, bool full = false);
 
 }  // namespace aidw

@@ -109,10 +109,17 @@ __global__ void __launch_bounds__(kBlock) fused_fixed_kernel(const FusedArgs a)
     InterpF32State<Q> st2;
 #pragma unroll
     for (int q = 0; q < Q; ++q) st2.init(q, qx[q], qy[q], al[q], d1[q]);
+    const int nblk = acc_blocks(nt);
+    int blk = 0, bend = nt + block_tile(1, nt, nblk);
     for (int t = nt; t < ntot; ++t) {
         ring.wait_full(t);
         const float *d = sm + ring.slot(t) * 5 * TILE;
         interp_f32_tile<Q, EMU, TILE>(st2, d, d + TILE, d + 2 * TILE);
+        if (t + 1 == bend) {  // accumulation-block boundary, as in the weighting kernel
+            st2.end_block();
+            ++blk;
+            bend = nt + block_tile(blk + 1, nt, nblk);
+        }
         ring.release(t, ntot, issue);
     }
 #pragma unroll

@@ -28,6 +28,7 @@ template <typename T> struct InterpArgs {
     T alpha_const;
     double *partial;  // nullable: data-sharded partial sums instead of z
     const int *perm;  // nullable: position i evaluates query perm[i] (class grouping)
+    double2 *bpart;   // split mode: per-accumulation-block sums [nblk][nq] (gridDim.y > 1)
 };
 
 // Weight math per precision: fp32 MUFU (scalar variant), fp64 table + polynomial
@@ -104,6 +105,11 @@ __global__ void __launch_bounds__(kBlock) interp_kernel(const InterpArgs<T> a)
         SWZ[q] = 0.0;
     }
 
+    const int nblk = acc_blocks(ntiles);
+    int blk = 0, bend = block_tile(1, ntiles, nblk);
+    double BW[Q], BWZ[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) BW[q] = BWZ[q] = 0.0;
     for (int t = 0; t < ntiles; ++t) {
         r.ring.wait_full(t);
         const int o = r.ring.slot(t) * TILE;
@@ -126,8 +132,18 @@ __global__ void __launch_bounds__(kBlock) interp_kernel(const InterpArgs<T> a)
         }
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            SW[q] += (double)sw[q];
-            SWZ[q] += (double)swz[q];
+            BW[q] += (double)sw[q];
+            BWZ[q] += (double)swz[q];
+        }
+        if (t + 1 == bend) {  // end of an accumulation block: block sums in block order
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                SW[q] += BW[q];
+                SWZ[q] += BWZ[q];
+                BW[q] = BWZ[q] = 0.0;
+            }
+            ++blk;
+            bend = block_tile(blk + 1, ntiles, nblk);
         }
         r.ring.release(t, ntiles, issue);
     }
@@ -147,7 +163,7 @@ constexpr int interp_min_blocks(int q) { return q == 1 ? 12 : q == 2 ? 9 : 6; }
 // (the generic XYZRing is shared with the fp64 kernel; its stage count is a template
 // parameter so the packed kernel can trade pipeline depth for occupancy)
 
-template <int Q, unsigned EMU, int STAGES = kStagesW, int BLOCK = kBlock>
+template <int Q, unsigned EMU, int STAGES = kStagesW, int BLOCK = kBlock, bool SPLIT = false>
 __global__ void __launch_bounds__(BLOCK, interp_min_blocks(Q) * kBlock / BLOCK)
     interp_f32x2_kernel(const InterpArgs<float> a)
 {
@@ -155,11 +171,15 @@ __global__ void __launch_bounds__(BLOCK, interp_min_blocks(Q) * kBlock / BLOCK)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     XYZRing<float, TILE, STAGES, BLOCK / 32> r(smem_raw);
     const int ntiles = (int)(a.ndp / TILE);
+    // split mode (gridDim.y = S > 1): this CTA covers accumulation blocks [b0, b1)
+    const int nblk = acc_blocks(ntiles), S = SPLIT ? (int)gridDim.y : 1;
+    const int b0 = SPLIT ? (int)blockIdx.y * nblk / S : 0, b1 = SPLIT ? ((int)blockIdx.y + 1) * nblk / S : nblk;
+    const int t0 = block_tile(b0, ntiles, nblk), nloc = block_tile(b1, ntiles, nblk) - t0;
     if (threadIdx.x == 0) r.ring.init();
     __syncthreads();
-    auto issue = [&](int tile, int slot) { r.issue(a, tile, slot); };
+    auto issue = [&](int tile, int slot) { r.issue(a, t0 + tile, slot); };
     if (threadIdx.x == 0)
-        for (int s = 0; s < STAGES && s < ntiles; ++s) issue(s, s);
+        for (int s = 0; s < STAGES && s < nloc; ++s) issue(s, s);
 
     const int64_t base = (int64_t)blockIdx.x * (BLOCK * Q) + threadIdx.x;
     float qx[Q], qy[Q], d1[Q];
@@ -189,7 +209,11 @@ __global__ void __launch_bounds__(BLOCK, interp_min_blocks(Q) * kBlock / BLOCK)
         cta_cls = n > 1 ? kClsMixed : any_1 ? kClsA1 : any_2 ? kClsA2 : any_3 ? kClsA3 : kClsGeneral;
     }
 
-    for (int t = 0; t < ntiles; ++t) {
+    __shared__ double2 acc_s[Q][BLOCK];  // per-thread running sums over blocks (unsplit)
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc_s[q][threadIdx.x] = make_double2(0.0, 0.0);
+    int blk = b0, bend = block_tile(b0 + 1, ntiles, nblk) - t0;
+    for (int t = 0; t < nloc; ++t) {
         r.ring.wait_full(t);
         const int o = r.ring.slot(t) * TILE;
         switch (cta_cls) {  // CTA-uniform
@@ -199,14 +223,49 @@ __global__ void __launch_bounds__(BLOCK, interp_min_blocks(Q) * kBlock / BLOCK)
         case kClsMixed: interp_f32_tile_cls<Q, kClsMixed, EMU, TILE>(st, cls, r.sx + o, r.sy + o, r.sz + o); break;
         default: interp_f32_tile<Q, EMU, TILE>(st, r.sx + o, r.sy + o, r.sz + o); break;
         }
-        r.ring.release(t, ntiles, issue);
+        if (t + 1 == bend) {  // end of an accumulation block
+            if constexpr (SPLIT) {
+#pragma unroll
+                for (int q = 0; q < Q; ++q)
+                    if (valid[q]) a.bpart[(int64_t)blk * a.nq + qid[q]] = make_double2(st.BW[q], st.BWZ[q]);
+#pragma unroll
+                for (int q = 0; q < Q; ++q) st.BW[q] = st.BWZ[q] = 0.0;
+            } else {  // block sums accumulate in smem (registers are at the occupancy cap)
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    acc_s[q][threadIdx.x].x += st.BW[q];
+                    acc_s[q][threadIdx.x].y += st.BWZ[q];
+                    st.BW[q] = st.BWZ[q] = 0.0;
+                }
+            }
+            ++blk;
+            bend = block_tile(blk + 1, ntiles, nblk) - t0;
+        }
+        r.ring.release(t, nloc, issue);
     }
 
+    if constexpr (!SPLIT) {
 #pragma unroll
-    for (int q = 0; q < Q; ++q)
-        if (valid[q])
-            write_result<float>(a.z, a.partial, qid[q], st.SW[q], st.SWZ[q], d1[q], qx[q], qy[q], a.px, a.py, a.pz,
-                                a.nd);
+        for (int q = 0; q < Q; ++q)
+            if (valid[q])
+                write_result<float>(a.z, a.partial, qid[q], acc_s[q][threadIdx.x].x, acc_s[q][threadIdx.x].y, d1[q],
+                                    qx[q], qy[q], a.px, a.py, a.pz, a.nd);
+    }
+}
+
+// Split mode: Z (or the data-sharded partials) from the per-block sums, added in block
+// order exactly as an unsplit launch adds them.
+__global__ void finalize_split_kernel(const InterpArgs<float> a, int nblk)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.nq; i += (int64_t)gridDim.x * blockDim.x) {
+        double SW = 0.0, SWZ = 0.0;
+        for (int b = 0; b < nblk; ++b) {
+            const double2 v = a.bpart[(int64_t)b * a.nq + i];
+            SW += v.x;
+            SWZ += v.y;
+        }
+        write_result<float>(a.z, a.partial, i, SW, SWZ, a.d1sq[i], a.qx[i], a.qy[i], a.px, a.py, a.pz, a.nd);
+    }
 }
 
 // Class grouping (2 small kernels): counts per class, then a scatter into perm in the
@@ -265,18 +324,72 @@ static int launch_interp_t(const InterpArgs<T> &a, cudaStream_t st)
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
+// Split factor for a launch of `grid` CTAs: 1 when the grid already fills `waves`
+// waves of resident CTAs, else enough data splits for ~`waves` waves (<= `maxs`), or
+// `maxs` itself when `full`.  AIDW_SPLIT=0 disables,
+// AIDW_SPLIT=n forces n (tests).
+static int split_env()
+{
+    const char *e = getenv("AIDW_SPLIT");  // read per launch so tests can toggle it
+    return e ? atoi(e) : -1;
+}
+
+int choose_split(const void *kern, int block, size_t smem, int64_t grid, int maxs, int waves, bool full)
+{
+    const int forced = split_env();
+    if (forced == 0) return 1;
+    if (forced > 0) return forced < maxs ? forced : maxs;
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 1;
+    }
+    const int64_t slots = (int64_t)occ * sms, target = waves * slots;
+    int64_t s = target / grid;  // floor: a partial extra wave costs more than it fills
+    if (s < 2) return 1;
+    if (full) return maxs;
+    return (int)(s < maxs ? s : maxs);
+}
+
+template <int Q, unsigned EMU, int STAGES, int BLOCK, bool SPLIT> static int interp_attrs(size_t smem)
+{
+    auto kern = interp_f32x2_kernel<Q, EMU, STAGES, BLOCK, SPLIT>;
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+                   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) == cudaSuccess
+               ? 0
+               : -1;
+}
+
 template <int Q, unsigned EMU, int STAGES = kStagesW, int BLOCK = kBlock>
-static int launch_interp_f32x2(const InterpArgs<float> &a, cudaStream_t st)
+static int launch_interp_f32x2(InterpArgs<float> a, cudaStream_t st, SplitBuf *split)
 {
     const size_t smem = XYZRing<float, kTileW, STAGES>::smem_bytes();
-    auto kern = interp_f32x2_kernel<Q, EMU, STAGES, BLOCK>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
-        return -1;
+    if (interp_attrs<Q, EMU, STAGES, BLOCK, false>(smem) < 0) return -1;
     const int64_t per_cta = (int64_t)BLOCK * Q;
     const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
-    kern<<<grid, BLOCK, smem, st>>>(a);
-    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+    const int nblk = acc_blocks((int)(a.ndp / kTileW));
+    // Weighting splits carry no per-split warm-up (unlike the kNN), so a full split into
+    // the nblk accumulation blocks is used whenever the grid is under 16 waves: it also
+    // removes the partial last wave (profiles/r01_split.jsonl).
+    int S = split ? choose_split((const void *)interp_f32x2_kernel<Q, EMU, STAGES, BLOCK, false>, BLOCK, smem, grid,
+                                 nblk, 16, true)
+                  : 1;
+    a.bpart = S > 1 ? static_cast<double2 *>(split->reserve((size_t)nblk * (size_t)a.nq * sizeof(double2)))
+                    : nullptr;
+    if (!a.bpart) S = 1;
+    if (S == 1) {
+        interp_f32x2_kernel<Q, EMU, STAGES, BLOCK, false><<<grid, BLOCK, smem, st>>>(a);
+        return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+    }
+    if (interp_attrs<Q, EMU, STAGES, BLOCK, true>(smem) < 0) return -1;
+    interp_f32x2_kernel<Q, EMU, STAGES, BLOCK, true><<<dim3(grid, (unsigned)S), BLOCK, smem, st>>>(a);
+    if (cudaPeekAtLastError() != cudaSuccess) return -1;
+    int64_t blocks = (a.nq + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    finalize_split_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, nblk);
+    return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 
 // Variant selection for tuning (AIDW_INTERP_VARIANT; tools/tune_interp.py); 0 = default.
@@ -290,30 +403,30 @@ static int interp_variant()
     return v;
 }
 
-static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st)
+static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st, SplitBuf *sp)
 {
     // EMU: 2-bit mode per couple h of 4-point group g at bit 4g+2h (passes.cuh)
     switch (interp_variant()) {
     case 1: return launch_interp_t<float, 2>(a, st);        // scalar, all-SFU
-    case 2: return launch_interp_f32x2<2, 0x0000>(a, st);   // packed, all-SFU
-    case 3: return launch_interp_f32x2<2, 0x1111>(a, st);   // 4 of 8 couples on the FMA pipe
-    case 4: return launch_interp_f32x2<2, 0xAAAA>(a, st);   // every couple split (f = 1/2)
-    case 5: return launch_interp_f32x2<2, 0x2A2A>(a, st);   // f = 3/8, split
-    case 6: return launch_interp_f32x2<2, 0x2222>(a, st);   // f = 1/4, split
-    case 7: return launch_interp_f32x2<2, 0x22A2>(a, st);   // f = 5/16, split
-    case 8: return launch_interp_f32x2<2, 0x1241>(a, st);   // f = 3/8, packed + one split
-    case 9: return launch_interp_f32x2<1, 0x0141>(a, st);   // Q = 1
-    case 10: return launch_interp_f32x2<3, 0x0141>(a, st);  // Q = 3
-    case 11: return launch_interp_f32x2<4, 0x0141>(a, st);  // Q = 4
-    case 12: return launch_interp_f32x2<1, 0x0141, 3>(a, st);  // Q = 1, 3 stages (12 CTAs/SM)
-    case 13: return launch_interp_f32x2<1, 0x0141, 2>(a, st);  // Q = 1, 2 stages
-    case 14: return launch_interp_f32x2<1, 0x1111, 3>(a, st);  // Q = 1, 3 stages, f = 1/2
-    case 15: return launch_interp_f32x2<2, 0x0141, 3>(a, st);  // Q = 2, 3 stages
-    case 16: return launch_interp_f32x2<2, 0x0141>(a, st);  // Q = 2
-    case 17: return launch_interp_f32x2<1, 0x0141, 4, 256>(a, st);  // Q = 1, 256-thread CTAs
-    case 18: return launch_interp_f32x2<1, 0x0141, 4, 512>(a, st);  // Q = 1, 512-thread CTAs
-    case 19: return launch_interp_f32x2<2, 0x0141, 4, 256>(a, st);  // Q = 2, 256-thread CTAs
-    default: return launch_interp_f32x2<1, 0x0141>(a, st); // Q = 1, f = 3/8 packed (best measured, r01)
+    case 2: return launch_interp_f32x2<2, 0x0000>(a, st, sp);   // packed, all-SFU
+    case 3: return launch_interp_f32x2<2, 0x1111>(a, st, sp);   // 4 of 8 couples on the FMA pipe
+    case 4: return launch_interp_f32x2<2, 0xAAAA>(a, st, sp);   // every couple split (f = 1/2)
+    case 5: return launch_interp_f32x2<2, 0x2A2A>(a, st, sp);   // f = 3/8, split
+    case 6: return launch_interp_f32x2<2, 0x2222>(a, st, sp);   // f = 1/4, split
+    case 7: return launch_interp_f32x2<2, 0x22A2>(a, st, sp);   // f = 5/16, split
+    case 8: return launch_interp_f32x2<2, 0x1241>(a, st, sp);   // f = 3/8, packed + one split
+    case 9: return launch_interp_f32x2<1, 0x0141>(a, st, sp);   // Q = 1
+    case 10: return launch_interp_f32x2<3, 0x0141>(a, st, sp);  // Q = 3
+    case 11: return launch_interp_f32x2<4, 0x0141>(a, st, sp);  // Q = 4
+    case 12: return launch_interp_f32x2<1, 0x0141, 3>(a, st, sp);  // Q = 1, 3 stages (12 CTAs/SM)
+    case 13: return launch_interp_f32x2<1, 0x0141, 2>(a, st, sp);  // Q = 1, 2 stages
+    case 14: return launch_interp_f32x2<1, 0x1111, 3>(a, st, sp);  // Q = 1, 3 stages, f = 1/2
+    case 15: return launch_interp_f32x2<2, 0x0141, 3>(a, st, sp);  // Q = 2, 3 stages
+    case 16: return launch_interp_f32x2<2, 0x0141>(a, st, sp);  // Q = 2
+    case 17: return launch_interp_f32x2<1, 0x0141, 4, 256>(a, st, sp);  // Q = 1, 256-thread CTAs
+    case 18: return launch_interp_f32x2<1, 0x0141, 4, 512>(a, st, sp);  // Q = 1, 512-thread CTAs
+    case 19: return launch_interp_f32x2<2, 0x0141, 4, 256>(a, st, sp);  // Q = 2, 256-thread CTAs
+    default: return launch_interp_f32x2<1, 0x0141>(a, st, sp); // Q = 1, f = 3/8 packed (best measured, r01)
     }
 }
 
@@ -347,13 +460,13 @@ int launch_finalize(int dtype, const double *partials, int P, int64_t nq, void *
 
 int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const void *qx,
                   const void *qy, int64_t nq, const void *alpha, double alpha_const, const void *d1sq, void *z,
-                  cudaStream_t st, double *partial, int *perm, unsigned *cls_counts)
+                  cudaStream_t st, double *partial, int *perm, unsigned *cls_counts, SplitBuf *split)
 {
     if (dtype == 0) {
         const float *p = static_cast<const float *>(data);
         InterpArgs<float> a{p, p + ndp, p + 2 * ndp, ndp, nd, (const float *)qx, (const float *)qy,
                             (const float *)alpha, (const float *)d1sq, nq, (float *)z, (float)alpha_const,
-                            partial, nullptr};
+                            partial, nullptr, nullptr};
         int launches = 0;
         if (perm && cls_counts && interp_variant() != 1) {
             if (cudaMemsetAsync(cls_counts, 0, 8 * sizeof(unsigned), st) != cudaSuccess) return -1;
@@ -365,13 +478,13 @@ int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const vo
             launches = 2;
             a.perm = perm;
         }
-        const int n = launch_interp_f32(a, st);
+        const int n = launch_interp_f32(a, st, split);
         return n < 0 ? -1 : n + launches;
     }
     const double *p = static_cast<const double *>(data);
     InterpArgs<double> a{p, p + ndp, p + 2 * ndp, ndp, nd, (const double *)qx, (const double *)qy,
                          (const double *)alpha, (const double *)d1sq, nq, (double *)z, alpha_const, partial,
-                         nullptr};
+                         nullptr, nullptr};
     return launch_interp_t<double, 2>(a, st);
 }
 

@@ -36,7 +36,36 @@ template <typename T> struct KnnArgs {
     T *r_obs, *d1sq, *minmax, *dists;  // all nullable except where the caller needs them
     Scratch *sc;
     int dists_sq;  // 1: dists receives the k squared distances s (data-sharded partial lists)
+    T *lists;      // split mode (gridDim.y = S > 1): per-split k smallest s, [S][nq][k] ascending
 };
+
+// Split mode: this CTA scans data tiles [t0, t0 + nloc) (blockIdx.y of gridDim.y equal
+// ranges); S = 1 covers everything.
+struct TileRange {
+    int t0, nloc;
+};
+__device__ __forceinline__ TileRange split_range(int ntiles)
+{
+    const int S = (int)gridDim.y, y = (int)blockIdx.y;
+    const int t0 = (int)((long long)y * ntiles / S), t1 = (int)((long long)(y + 1) * ntiles / S);
+    return {t0, t1 - t0};
+}
+
+// Split-mode epilogue: the CTA's ascending k smallest squared distances per query.
+template <typename T, int K, int Q>
+__device__ __forceinline__ void knn_write_split(const KnnArgs<T> &a, T (&buf)[Q][K], const bool (&valid)[Q],
+                                                int64_t base, int k0)
+{
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int64_t idx = base + q * kBlock;
+        if (!valid[q]) continue;
+        T *o = a.lists + ((int64_t)blockIdx.y * a.nq + idx) * a.k;
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            if (i >= k0) o[i - k0] = buf[q][i];
+    }
+}
 
 template <typename T> __device__ __forceinline__ T from_bits(unsigned long long b);
 template <> __device__ __forceinline__ float from_bits<float>(unsigned long long b) { return __uint_as_float((unsigned)b); }
@@ -144,7 +173,7 @@ __device__ __forceinline__ void knn_epilogue(const KnnArgs<T> &a, T (&buf)[Q][K]
 // ---------------------------------------------------------------------------------
 // Canonical kernel: every pair evaluated with the R16 sequence (fp64 path; fp32 with
 // AIDW_KNN_FILTER=0).  4 FP32/FP64 ops + 1 compare per pair.
-template <typename T, int K, int Q>
+template <typename T, int K, int Q, bool SPLIT>
 __global__ void __launch_bounds__(kBlock) knn_robs_kernel(const KnnArgs<T> a)
 {
     constexpr int TILE = kTileK, STAGES = kStagesK;
@@ -153,14 +182,16 @@ __global__ void __launch_bounds__(kBlock) knn_robs_kernel(const KnnArgs<T> a)
     T *sy = sx + STAGES * TILE;
     Ring<STAGES> ring{reinterpret_cast<uint64_t *>(sy + STAGES * TILE),
                       reinterpret_cast<uint64_t *>(sy + STAGES * TILE) + STAGES};
-    const int ntiles = (int)(a.ndp / TILE);
+    const TileRange tr = SPLIT ? split_range((int)(a.ndp / TILE)) : TileRange{0, (int)(a.ndp / TILE)};
+    const int ntiles = tr.nloc;
     if (threadIdx.x == 0) ring.init();
     __syncthreads();
 
     auto issue = [&](int tile, int slot) {
+        const int64_t off = (int64_t)(tr.t0 + tile) * TILE;
         mbar_arrive_expect_tx(&ring.full[slot], 2u * TILE * sizeof(T));
-        bulk_g2s(sx + slot * TILE, a.px + (int64_t)tile * TILE, TILE * sizeof(T), &ring.full[slot]);
-        bulk_g2s(sy + slot * TILE, a.py + (int64_t)tile * TILE, TILE * sizeof(T), &ring.full[slot]);
+        bulk_g2s(sx + slot * TILE, a.px + off, TILE * sizeof(T), &ring.full[slot]);
+        bulk_g2s(sy + slot * TILE, a.py + off, TILE * sizeof(T), &ring.full[slot]);
     };
     if (threadIdx.x == 0)
         for (int s = 0; s < STAGES && s < ntiles; ++s) issue(s, s);
@@ -208,12 +239,15 @@ __global__ void __launch_bounds__(kBlock) knn_robs_kernel(const KnnArgs<T> a)
         }
         ring.release(t, ntiles, issue);
     }
-    knn_epilogue<T, K, Q>(a, buf, valid, base, k0);
+    if constexpr (SPLIT)
+        knn_write_split<T, K, Q>(a, buf, valid, base, k0);
+    else
+        knn_epilogue<T, K, Q>(a, buf, valid, base, k0);
 }
 
 // ---------------------------------------------------------------------------------
 // Filtered fp32 kernel (passes.cuh knn_f32_tile): smem tiles of (cx, cy, pp, x, y).
-template <int K, int Q, int G>
+template <int K, int Q, int G, bool SPLIT>
 __global__ void __launch_bounds__(kBlock) knn_filter_kernel(const KnnArgs<float> a, const FilterArgs f)
 {
     constexpr int TILE = kTileKF, STAGES = kStagesKF;
@@ -225,14 +259,15 @@ __global__ void __launch_bounds__(kBlock) knn_filter_kernel(const KnnArgs<float>
     float *spy = spx + STAGES * TILE;
     Ring<STAGES> ring{reinterpret_cast<uint64_t *>(spy + STAGES * TILE),
                       reinterpret_cast<uint64_t *>(spy + STAGES * TILE) + STAGES};
-    const int ntiles = (int)(a.ndp / TILE);
+    const TileRange tr = SPLIT ? split_range((int)(a.ndp / TILE)) : TileRange{0, (int)(a.ndp / TILE)};
+    const int ntiles = tr.nloc;
     if (threadIdx.x == 0) ring.init();
     __syncthreads();
 
     auto issue = [&](int tile, int slot) {
         constexpr uint32_t B = TILE * sizeof(float);
         mbar_arrive_expect_tx(&ring.full[slot], 5u * B);
-        const int64_t off = (int64_t)tile * TILE;
+        const int64_t off = (int64_t)(tr.t0 + tile) * TILE;
         bulk_g2s(scx + slot * TILE, f.cx + off, B, &ring.full[slot]);
         bulk_g2s(scy + slot * TILE, f.cy + off, B, &ring.full[slot]);
         bulk_g2s(spp + slot * TILE, f.pp + off, B, &ring.full[slot]);
@@ -257,23 +292,63 @@ __global__ void __launch_bounds__(kBlock) knn_filter_kernel(const KnnArgs<float>
         knn_f32_tile<K, Q, G, TILE>(st, scx + o, scy + o, spp + o, spx + o, spy + o);
         ring.release(t, ntiles, issue);
     }
-    knn_epilogue<float, K, Q>(a, st.buf, valid, base, k0);
+    if constexpr (SPLIT)
+        knn_write_split<float, K, Q>(a, st.buf, valid, base, k0);
+    else
+        knn_epilogue<float, K, Q>(a, st.buf, valid, base, k0);
 }
 
 // ---------------------------------------------------------------------------------
+// Small-nq data split: when the query grid leaves SMs idle, the data
+// tiles are split across gridDim.y; each split writes its k smallest s and the merge
+// kernel (N4's) forms the exact job-wide list and the usual epilogue.
+template <typename T> static int dispatch_merge(const KnnArgs<T> &a, const T *lists, int P, cudaStream_t st);
+
+template <typename T>
+static int knn_split_factor(const void *kern, size_t smem, unsigned grid, int ntiles, KnnArgs<T> &a, SplitBuf *sp)
+{
+    a.lists = nullptr;
+    if (!sp) return 1;
+    const int S = choose_split(kern, kBlock, smem, grid, ntiles, 1);
+    if (S <= 1) return 1;
+    a.lists = static_cast<T *>(sp->reserve((size_t)S * (size_t)a.nq * (size_t)a.k * sizeof(T)));
+    return a.lists ? S : 1;
+}
+
+template <typename T> static int knn_finish(const KnnArgs<T> &a, int S, cudaStream_t st)
+{
+    if (cudaPeekAtLastError() != cudaSuccess) return -1;
+    if (S == 1) return 1;
+    const int n = dispatch_merge<T>(a, a.lists, S, st);
+    return n < 0 ? -1 : 1 + n;
+}
+
+// ---------------------------------------------------------------------------------
+template <int K, int Q, int G, bool SPLIT> static int set_filter_attrs(size_t smem)
+{
+    auto kern = knn_filter_kernel<K, Q, G, SPLIT>;
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+                   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) == cudaSuccess
+               ? 0
+               : -1;
+}
+
 template <int K, int Q, int G = 8>
-static int launch_knn_filter_t(const KnnArgs<float> &a, const FilterArgs &f, cudaStream_t st)
+static int launch_knn_filter_t(KnnArgs<float> a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp)
 {
     const size_t smem = (size_t)5 * kStagesKF * kTileKF * sizeof(float) + 2 * kStagesKF * sizeof(uint64_t);
-    if (cudaFuncSetAttribute(knn_filter_kernel<K, Q, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess ||
-        cudaFuncSetAttribute(knn_filter_kernel<K, Q, G>, cudaFuncAttributePreferredSharedMemoryCarveout, 100) !=
-            cudaSuccess)
-        return -1;
+    if (set_filter_attrs<K, Q, G, false>(smem) < 0) return -1;
     const int64_t per_cta = (int64_t)kBlock * Q;
     const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
-    knn_filter_kernel<K, Q, G><<<grid, kBlock, smem, st>>>(a, f);
-    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+    const int S =
+        knn_split_factor((const void *)knn_filter_kernel<K, Q, G, false>, smem, grid, (int)(a.ndp / kTileKF), a, sp);
+    if (S == 1) {
+        knn_filter_kernel<K, Q, G, false><<<grid, kBlock, smem, st>>>(a, f);
+    } else {
+        if (set_filter_attrs<K, Q, G, true>(smem) < 0) return -1;
+        knn_filter_kernel<K, Q, G, true><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, f);
+    }
+    return knn_finish(a, S, st);
 }
 
 static int knn_variant()
@@ -286,31 +361,31 @@ static int knn_variant()
     return v;
 }
 
-static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaStream_t st)
+static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp)
 {
     const int k = a.k;
     if (k <= 10 && k > 8) {
         switch (knn_variant()) {  // tuning sweep (tools/tune_knn.py)
-        case 2: return launch_knn_filter_t<10, 4, 8>(a, f, st);
-        case 3: return launch_knn_filter_t<10, 2, 16>(a, f, st);
-        case 4: return launch_knn_filter_t<10, 2, 8>(a, f, st);
-        case 5: return launch_knn_filter_t<10, 3, 16>(a, f, st);
-        case 6: return launch_knn_filter_t<10, 4, 16>(a, f, st);
-        case 7: return launch_knn_filter_t<10, 2, 32>(a, f, st);
+        case 2: return launch_knn_filter_t<10, 4, 8>(a, f, st, sp);
+        case 3: return launch_knn_filter_t<10, 2, 16>(a, f, st, sp);
+        case 4: return launch_knn_filter_t<10, 2, 8>(a, f, st, sp);
+        case 5: return launch_knn_filter_t<10, 3, 16>(a, f, st, sp);
+        case 6: return launch_knn_filter_t<10, 4, 16>(a, f, st, sp);
+        case 7: return launch_knn_filter_t<10, 2, 32>(a, f, st, sp);
         default: break;
         }
     }
     // Q = 2 queries per thread, G = 16 points per warp vote (best measured, r01)
-    if (k <= 1) return launch_knn_filter_t<1, 2, 16>(a, f, st);
-    if (k <= 2) return launch_knn_filter_t<2, 2, 16>(a, f, st);
-    if (k <= 4) return launch_knn_filter_t<4, 2, 16>(a, f, st);
-    if (k <= 8) return launch_knn_filter_t<8, 2, 16>(a, f, st);
-    if (k <= 10) return launch_knn_filter_t<10, 2, 16>(a, f, st);
-    if (k <= 12) return launch_knn_filter_t<12, 2, 16>(a, f, st);
-    if (k <= 15) return launch_knn_filter_t<15, 2, 16>(a, f, st);
-    if (k <= 16) return launch_knn_filter_t<16, 2, 16>(a, f, st);
-    if (k <= 24) return launch_knn_filter_t<24, 2>(a, f, st);
-    return launch_knn_filter_t<32, 2>(a, f, st);
+    if (k <= 1) return launch_knn_filter_t<1, 2, 16>(a, f, st, sp);
+    if (k <= 2) return launch_knn_filter_t<2, 2, 16>(a, f, st, sp);
+    if (k <= 4) return launch_knn_filter_t<4, 2, 16>(a, f, st, sp);
+    if (k <= 8) return launch_knn_filter_t<8, 2, 16>(a, f, st, sp);
+    if (k <= 10) return launch_knn_filter_t<10, 2, 16>(a, f, st, sp);
+    if (k <= 12) return launch_knn_filter_t<12, 2, 16>(a, f, st, sp);
+    if (k <= 15) return launch_knn_filter_t<15, 2, 16>(a, f, st, sp);
+    if (k <= 16) return launch_knn_filter_t<16, 2, 16>(a, f, st, sp);
+    if (k <= 24) return launch_knn_filter_t<24, 2>(a, f, st, sp);
+    return launch_knn_filter_t<32, 2>(a, f, st, sp);
 }
 
 // ---------------------------------------------------------------------------------
@@ -349,7 +424,7 @@ static int launch_merge_k(const KnnArgs<T> &a, const T *lists, int P, cudaStream
 
 template <typename T>
 static int dispatch_merge(const KnnArgs<T> &a, const T *lists, int P, cudaStream_t st)
-{
+{  // a.lists is not read by the merge kernel
     const int k = a.k;
     if (k <= 1) return launch_merge_k<T, 1>(a, lists, P, st);
     if (k <= 2) return launch_merge_k<T, 2>(a, lists, P, st);
@@ -368,11 +443,11 @@ int launch_knn_merge(int dtype, int k, const void *lists, int P, int64_t nq, voi
 {
     if (dtype == 0) {
         KnnArgs<float> a{nullptr, nullptr, 0, nullptr, nullptr, nq, k, (float *)r_obs, (float *)d1sq,
-                         (float *)minmax, nullptr, sc, 0};
+                         (float *)minmax, nullptr, sc, 0, nullptr};
         return dispatch_merge(a, (const float *)lists, P, st);
     }
     KnnArgs<double> a{nullptr, nullptr, 0, nullptr, nullptr, nq, k, (double *)r_obs, (double *)d1sq,
-                      (double *)minmax, nullptr, sc, 0};
+                      (double *)minmax, nullptr, sc, 0, nullptr};
     return dispatch_merge(a, (const double *)lists, P, st);
 }
 
@@ -383,53 +458,62 @@ template <typename T> __global__ void minmax_identity_kernel(T *mm)
 }
 
 template <typename T, int K, int Q>
-static int launch_knn_t(const KnnArgs<T> &a, cudaStream_t st)
+static int launch_knn_t(KnnArgs<T> a, cudaStream_t st, SplitBuf *sp)
 {
     const size_t smem = (size_t)2 * kStagesK * kTileK * sizeof(T) + 2 * kStagesK * sizeof(uint64_t);
-    if (cudaFuncSetAttribute(knn_robs_kernel<T, K, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(knn_robs_kernel<T, K, Q, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return -1;
     const int64_t per_cta = (int64_t)kBlock * Q;
     const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
-    knn_robs_kernel<T, K, Q><<<grid, kBlock, smem, st>>>(a);
-    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+    const int S =
+        knn_split_factor((const void *)knn_robs_kernel<T, K, Q, false>, smem, grid, (int)(a.ndp / kTileK), a, sp);
+    if (S == 1) {
+        knn_robs_kernel<T, K, Q, false><<<grid, kBlock, smem, st>>>(a);
+    } else {
+        if (cudaFuncSetAttribute(knn_robs_kernel<T, K, Q, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+            return -1;
+        knn_robs_kernel<T, K, Q, true><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a);
+    }
+    return knn_finish(a, S, st);
 }
 
 template <typename T>
-static int dispatch_k(const KnnArgs<T> &a, cudaStream_t st)
+static int dispatch_k(const KnnArgs<T> &a, cudaStream_t st, SplitBuf *sp)
 {
     const int k = a.k;
-    if (k <= 1) return launch_knn_t<T, 1, 2>(a, st);
-    if (k <= 2) return launch_knn_t<T, 2, 2>(a, st);
-    if (k <= 4) return launch_knn_t<T, 4, 2>(a, st);
-    if (k <= 8) return launch_knn_t<T, 8, 2>(a, st);
-    if (k <= 10) return launch_knn_t<T, 10, 2>(a, st);
-    if (k <= 12) return launch_knn_t<T, 12, 2>(a, st);
-    if (k <= 15) return launch_knn_t<T, 15, 2>(a, st);
-    if (k <= 16) return launch_knn_t<T, 16, 2>(a, st);
-    if (k <= 24) return launch_knn_t<T, 24, 1>(a, st);
-    return launch_knn_t<T, 32, 1>(a, st);
+    if (k <= 1) return launch_knn_t<T, 1, 2>(a, st, sp);
+    if (k <= 2) return launch_knn_t<T, 2, 2>(a, st, sp);
+    if (k <= 4) return launch_knn_t<T, 4, 2>(a, st, sp);
+    if (k <= 8) return launch_knn_t<T, 8, 2>(a, st, sp);
+    if (k <= 10) return launch_knn_t<T, 10, 2>(a, st, sp);
+    if (k <= 12) return launch_knn_t<T, 12, 2>(a, st, sp);
+    if (k <= 15) return launch_knn_t<T, 15, 2>(a, st, sp);
+    if (k <= 16) return launch_knn_t<T, 16, 2>(a, st, sp);
+    if (k <= 24) return launch_knn_t<T, 24, 1>(a, st, sp);
+    return launch_knn_t<T, 32, 1>(a, st, sp);
 }
 
 int launch_knn(int dtype, int k, const void *data, int64_t ndp, const void *qx, const void *qy,
                int64_t nq, void *r_obs, void *d1sq, void *minmax, void *dists, Scratch *sc,
-               const FilterData *filt, cudaStream_t st, int dists_sq)
+               const FilterData *filt, cudaStream_t st, int dists_sq, SplitBuf *sp)
 {
     if (dtype == 0) {
         const float *p = static_cast<const float *>(data);
         KnnArgs<float> a{p, p + ndp, ndp, (const float *)qx, (const float *)qy, nq, k,
-                         (float *)r_obs, (float *)d1sq, (float *)minmax, (float *)dists, sc, dists_sq};
+                         (float *)r_obs, (float *)d1sq, (float *)minmax, (float *)dists, sc, dists_sq, nullptr};
         if (filt && filt->arrays) {
             const float *c = static_cast<const float *>(filt->arrays);
             FilterArgs f{c, c + ndp, c + 2 * ndp, filt->c_x, filt->c_y, filt->r1};
-            return dispatch_filter_k(a, f, st);
+            return dispatch_filter_k(a, f, st, sp);
         }
-        return dispatch_k(a, st);
+        return dispatch_k(a, st, sp);
     }
     const double *p = static_cast<const double *>(data);
     KnnArgs<double> a{p, p + ndp, ndp, (const double *)qx, (const double *)qy, nq, k,
-                      (double *)r_obs, (double *)d1sq, (double *)minmax, (double *)dists, sc, dists_sq};
-    return dispatch_k(a, st);
+                      (double *)r_obs, (double *)d1sq, (double *)minmax, (double *)dists, sc, dists_sq, nullptr};
+    return dispatch_k(a, st, sp);
 }
 
 int launch_minmax_identity(int dtype, void *minmax, cudaStream_t st)

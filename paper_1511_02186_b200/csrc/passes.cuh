@@ -281,7 +281,8 @@ __device__ __forceinline__ double alpha_eq(double robs, double r_exp, double rmi
 template <int Q>
 struct InterpF32State {
     f32x2 QX[Q], QY[Q], C[Q], B[Q];
-    double SW[Q], SWZ[Q];
+    double SW[Q], SWZ[Q];  // job sums: block sums added in block order (R21)
+    double BW[Q], BWZ[Q];  // current accumulation block
 
     __device__ __forceinline__ void init(int q, float x, float y, float alpha, float d1sq)
     {
@@ -293,8 +294,22 @@ struct InterpF32State {
         B[q] = splat2(b);
         SW[q] = 0.0;
         SWZ[q] = 0.0;
+        BW[q] = 0.0;
+        BWZ[q] = 0.0;
+    }
+    __device__ __forceinline__ void end_block()
+    {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            SW[q] += BW[q];
+            SWZ[q] += BWZ[q];
+            BW[q] = 0.0;
+            BWZ[q] = 0.0;
+        }
     }
 };
+
+
 
 // One smem tile of the fp32 weighting pass with packed fp32x2 arithmetic.  Two
 // consecutive data points of one query form a "couple" in one register pair; the fp32
@@ -360,8 +375,8 @@ __device__ __forceinline__ void interp_f32_tile(InterpF32State<Q> &st, const flo
     }
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        st.SW[q] += (double)sw[q].x + (double)sw[q].y;
-        st.SWZ[q] += (double)swz[q].x + (double)swz[q].y;
+        st.BW[q] += (double)sw[q].x + (double)sw[q].y;
+        st.BWZ[q] += (double)swz[q].x + (double)swz[q].y;
     }
 }
 
@@ -459,8 +474,8 @@ __device__ __forceinline__ void interp_f32_tile_cls(InterpF32State<Q> &st, const
     }
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        st.SW[q] += (double)sw[q].x + (double)sw[q].y;
-        st.SWZ[q] += (double)swz[q].x + (double)swz[q].y;
+        st.BW[q] += (double)sw[q].x + (double)sw[q].y;
+        st.BWZ[q] += (double)swz[q].x + (double)swz[q].y;
     }
 }
 

@@ -267,6 +267,35 @@ def test_sharding_bit_identical(P):
         assert np.array_equal(np.concatenate(zs), ref), world
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("nd,nq,k", [(3000, 500, 10), (30000, 4099, 15), (100003, 20000, 10), (262144, 1, 32),
+                                     (5000, 777, 1)])
+def test_split_bit_identical(P, monkeypatch, dtype, nd, nq, k):
+    """Small-nq data split (DESIGN.md §4.6) -- kNN: per-split k lists merged exactly;
+    weighting: per-accumulation-block sums added in block order by a finalize kernel --
+    gives bit-identical results to the unsplit launches, for every split factor, in
+    run / knn dists / idw / data-sharded partials; coincident queries included."""
+    x, y, z, qx, qy = datagen.random_cloud(300 + nq, nd, nq)
+    qx[::7], qy[::7] = x[: len(qx[::7])], y[: len(qy[::7])]
+    eng = P.AIDW(x, y, z, dtype=dtype)
+    outs = {}
+    for sv in ("0", "2", "3", "16", "1000", None):
+        if sv is None:
+            monkeypatch.delenv("AIDW_SPLIT", raising=False)
+        else:
+            monkeypatch.setenv("AIDW_SPLIT", sv)
+        zr, tr = eng.run(qx, qy, k, LV, P.GLOBAL, trace=True)
+        r, d1, mm, dd = eng.knn_robs(qx, qy, k, want_dists=True)
+        zi = eng.idw(qx, qy, 2.5)
+        a = eng.alpha(r, LV, P.GLOBAL, 0, 0, mm)
+        pp = eng.interpolate_partial(qx, qy, a, d1)
+        kp = eng.knn_partial(qx, qy, k)
+        outs[sv] = [t.cpu().numpy() for t in (zr, tr["r_obs"], tr["d1sq"], tr["minmax"], dd, zi, pp, kp)]
+    for sv, o in outs.items():
+        for n, (u, v) in enumerate(zip(o, outs["0"])):
+            assert np.array_equal(u, v, equal_nan=True), (sv, n)
+
+
 def test_errors(P):
     x, y, z, qx, qy = datagen.random_cloud(1, 100, 10)
     with pytest.raises(P.AidwError, match="DEGENERATE"):
@@ -301,13 +330,19 @@ def test_run_host_matches_device(P):
     assert torch.equal(zd, zh)
 
 
-def test_launch_count(P):
+def test_launch_count(P, monkeypatch):
     x, y, z, qx, qy = datagen.random_cloud(43, 3000, 500)
     eng = P.AIDW(x, y, z)
+    monkeypatch.setenv("AIDW_SPLIT", "0")
     n0 = eng.launches
     eng.run(qx, qy, 10)
     # knn_robs, alpha, class count + scatter (exact-exponent grouping), interpolate
     assert eng.launches - n0 == 5
+    monkeypatch.delenv("AIDW_SPLIT")
+    n0 = eng.launches
+    eng.run(qx, qy, 10)  # 500 queries leave SMs idle: split kNN + merge, split weighting + finalize
+    assert eng.launches - n0 == 7
+    monkeypatch.setenv("AIDW_SPLIT", "0")
     e64 = P.AIDW(x, y, z, dtype=torch.float64)
     n0 = e64.launches
     e64.run(qx, qy, 10)
@@ -317,9 +352,10 @@ def test_launch_count(P):
 # ------------------------------------------------------------------ N1 / N2
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 @pytest.mark.parametrize("k", [10, 15, 1])
-def test_run_fixed_fused(P, orc, dtype, k):
+def test_run_fixed_fused(P, orc, dtype, k, monkeypatch):
     """N1: one fused launch == the three stage kernels in FIXED mode (bit-identical),
     and within tolerance of the oracle."""
+    monkeypatch.setenv("AIDW_SPLIT", "0")  # launch count below: no small-nq data split
     x, y, z, qx, qy = datagen.random_cloud(50 + k, 7001, 1333)
     eng = P.AIDW(x, y, z, dtype=dtype)
     n0 = eng.launches
