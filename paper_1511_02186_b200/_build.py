@@ -9,7 +9,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libaidw.so")
-SOURCES = ["aidw_api.cu", "knn_robs.cu", "interpolate.cu", "alpha_prep.cu", "fused.cu", "paper_kernels.cu"]
+SOURCES = ["aidw_api.cu", "knn_robs.cu", "interpolate.cu", "alpha_prep.cu", "fused.cu", "paper_kernels.cu", "order.cu"]
 HEADERS = ["aidw_internal.h", "device.cuh", "packed.cuh", "passes.cuh", "f64_tables.h"]
 
 NVCC_FLAGS = [

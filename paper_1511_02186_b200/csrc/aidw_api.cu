@@ -289,7 +289,8 @@ aidw_status aidw_create(aidw_t *out, int device, aidw_dtype dt, aidw_layout lay,
         // r1 >= max |x - c_x| + |y - c_y| over the data (fp64, padded for fp32 rounding)
         const char *env = getenv("AIDW_KNN_FILTER");
         if (!(env && env[0] == '0')) {
-            if ((e = cudaMalloc(&h->filt.arrays, 3 * (size_t)h->ndp * sizeof(float))) != cudaSuccess) {
+            if ((e = cudaMalloc(&h->filt.arrays, 8 * (size_t)h->ndp * sizeof(float))) != cudaSuccess ||
+                (e = cudaMalloc(&h->filt.cell_start, (aidw::kCells + 1) * sizeof(int))) != cudaSuccess) {
                 cudaGetLastError();
                 return bail(fail(h, AIDW_E_NOMEM, "cudaMalloc filter: %s", cudaGetErrorString(e)));
             }
@@ -298,10 +299,13 @@ aidw_status aidw_create(aidw_t *out, int device, aidw_dtype dt, aidw_layout lay,
             const double rx = std::fmax(std::fabs(x0 - h->filt.c_x), std::fabs(x1 - h->filt.c_x));
             const double ry = std::fmax(std::fabs(y0 - h->filt.c_y), std::fabs(y1 - h->filt.c_y));
             h->filt.r1 = (float)((rx + ry) * (1.0 + 1e-6));
-            s = launched(h, aidw::launch_center(h->data, h->ndp, nd, h->filt.c_x, h->filt.c_y, h->filt.arrays, st),
-                         "center kernel");
+            // Morton order grid over the data bbox
+            constexpr double cells = (double)(1 << aidw::kOrderBits);
+            h->filt.grid = aidw::OrderGrid{(float)x0, (float)y0, (float)(cells / (x1 - x0)),
+                                           (float)(cells / (y1 - y0))};
+            s = launched(h, aidw::launch_order_data(h->data, h->ndp, nd, &h->filt, st), "order data kernels");
             if (s != AIDW_OK) return bail(s);
-            if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return bail(cuda_fail(h, e, "center sync"));
+            if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return bail(cuda_fail(h, e, "order data sync"));
         }
     }
     *out = h;
@@ -609,6 +613,8 @@ aidw_status aidw_destroy(aidw_t h)
     if (h->sc) cudaFree(h->sc);
     if (h->work) cudaFree(h->work);
     if (h->filt.arrays) cudaFree(h->filt.arrays);
+    if (h->filt.cell_start) cudaFree(h->filt.cell_start);
+    if (h->filt.qorder.p) cudaFree(h->filt.qorder.p);
     if (h->perm) cudaFree(h->perm);
     if (h->split.p) cudaFree(h->split.p);
     delete h;

@@ -51,12 +51,41 @@ struct Scratch {
     unsigned cls[8];            // weighting-pass class counts + cursors (launch_interp)
 };
 
-// fp32 kNN filter data owned by a handle: centred coordinates and
-// |p'|^2, [3][ndp] floats padded with +inf, the centre and the bound R1.
+// Spatial (Morton) order of points and queries for the fp32 kNN:
+// 2^kOrderBits x 2^kOrderBits cells over the data bbox; cell(x, y) clamps outside points
+// (and NaN) to the border, so any input maps to a cell.
+constexpr int kOrderBits = 8;
+constexpr int kCells = 1 << (2 * kOrderBits);
+struct OrderGrid {
+    float x0, y0, sx, sy;  // cell coordinate = (x - x0) * sx, clamped to [0, 2^bits - 1]
+};
+__host__ __device__ inline unsigned morton_cell(float x, float y, OrderGrid g)
+{
+    constexpr float top = (float)((1 << kOrderBits) - 1);
+    const float fx = fminf(fmaxf((x - g.x0) * g.sx, 0.f), top);  // NaN -> 0
+    const float fy = fminf(fmaxf((y - g.y0) * g.sy, 0.f), top);
+    unsigned ix = (unsigned)fx, iy = (unsigned)fy, c = 0;
+    for (int b = 0; b < kOrderBits; ++b) c |= ((ix >> b) & 1u) << (2 * b) | ((iy >> b) & 1u) << (2 * b + 1);
+    return c;
+}
+
+// fp32 kNN filter data owned by a handle: [8][ndp] floats padded
+// with +inf -- centred cx, cy, |p'|^2 in the caller's order, then the same three and
+// x, y in Morton order -- the centre, the bound R1, the order grid and each cell's first
+// sorted position.
 struct FilterData {
     void *arrays = nullptr;
     float c_x = 0.f, c_y = 0.f, r1 = 0.f;
+    int *cell_start = nullptr;  // [kCells + 1]
+    OrderGrid grid{0.f, 0.f, 0.f, 0.f};
+    SplitBuf qorder;            // per-call query order: counts, cursors, perm
 };
+
+// Morton-sort the data into the filter arrays (3 launches) and order a query batch
+// (perm[i] = query of launch slot i; 3 launches + a memset; scratch from `buf`).
+int launch_order_data(const void *data, int64_t ndp, int64_t nd, FilterData *fd, cudaStream_t st);
+int launch_order_queries(const float *qx, const float *qy, int64_t nq, const FilterData *fd, SplitBuf *buf,
+                         const int **perm, cudaStream_t st);
 
 // Each launcher returns the number of kernels it launched (>= 0) or -1 on a
 // launch error (cudaGetLastError is left set for the caller).
@@ -65,15 +94,12 @@ int launch_prep(int dtype, int layout, const void *src, int64_t nd, int64_t ndp,
 
 int launch_knn(int dtype, int k, const void *data, int64_t ndp, const void *qx, const void *qy,
                int64_t nq, void *r_obs, void *d1sq, void *minmax, void *dists, Scratch *sc,
-               const FilterData *filt, cudaStream_t st, int dists_sq = 0, SplitBuf *split = nullptr);
+               FilterData *filt, cudaStream_t st, int dists_sq = 0, SplitBuf *split = nullptr);
 
 int launch_knn_merge(int dtype, int k, const void *lists, int P, int64_t nq, void *r_obs, void *d1sq,
                      void *minmax, Scratch *sc, cudaStream_t st);
 
 int launch_finalize(int dtype, const double *partials, int P, int64_t nq, void *z, cudaStream_t st);
-
-int launch_center(const void *data, int64_t ndp, int64_t nd, float c_x, float c_y, void *filt,
-                  cudaStream_t st);
 
 int launch_minmax_identity(int dtype, void *minmax, cudaStream_t st);
 

@@ -104,33 +104,6 @@ int launch_prep(int dtype, int layout, const void *src, int64_t nd, int64_t ndp,
 
 // Centred fp32 copies and |p'|^2 for the kNN filter (knn_robs.cu): cx = x - c_x,
 // cy = y - c_y (RN), pp = fma(cx, cx, cy*cy); padding (+inf).
-__global__ void center_kernel(const float *__restrict__ data, int64_t ndp, int64_t nd, float c_x, float c_y,
-                              float *__restrict__ filt)
-{
-    const float *px = data, *py = data + ndp;
-    float *cx = filt, *cy = filt + ndp, *pp = filt + 2 * ndp;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndp;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        if (i < nd) {
-            const float a = __fsub_rn(px[i], c_x), b = __fsub_rn(py[i], c_y);
-            cx[i] = a;
-            cy[i] = b;
-            pp[i] = __fmaf_rn(a, a, __fmul_rn(b, b));
-        } else {
-            cx[i] = cy[i] = pp[i] = pos_inf<float>();
-        }
-    }
-}
-
-int launch_center(const void *data, int64_t ndp, int64_t nd, float c_x, float c_y, void *filt, cudaStream_t st)
-{
-    const int threads = 256;
-    int64_t blocks = (ndp + threads - 1) / threads;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    center_kernel<<<(unsigned)blocks, threads, 0, st>>>((const float *)data, ndp, nd, c_x, c_y, (float *)filt);
-    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
-}
-
 // ------------------------------------------------------------------ S4: alpha
 // Eq. 4-6 per query in fp64 (passes.cuh alpha_eq); GLOBAL bounds read on the device.
 template <typename T>

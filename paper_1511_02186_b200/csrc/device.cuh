@@ -85,6 +85,48 @@ __device__ __forceinline__ float ex2_approx(float x)
     return y;
 }
 
+// A value the compiler cannot rematerialise from its inputs (it stays in a register).
+__device__ __forceinline__ float opaque(float x)
+{
+    float r;
+    asm volatile("mov.b32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// Three-input fp32 min (sm_100 FMNMX3; NaN inputs are ignored like fminf's).
+__device__ __forceinline__ float fmin3(float a, float b, float c)
+{
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// Minimum of N values as a tree of 3-input mins (N = 16: 8 instructions, depth 3).
+template <int N> __device__ __forceinline__ float min_tree3(const float (&t)[N])
+{
+    float v[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = t[i];
+    int n = N;
+#pragma unroll
+    for (int level = 0; level < 8; ++level) {
+        if (n == 1) break;
+        int o = 0;
+#pragma unroll
+        for (int i = 0; i < N; i += 3) {
+            if (i >= n) break;
+            if (i + 2 < n)
+                v[o++] = fmin3(v[i], v[i + 1], v[i + 2]);
+            else if (i + 1 < n)
+                v[o++] = fminf(v[i], v[i + 1]);
+            else
+                v[o++] = v[i];
+        }
+        n = o;
+    }
+    return v[0];
+}
+
 __device__ __forceinline__ float rsqrt_approx(float x)
 {
     float y;
@@ -133,6 +175,16 @@ __device__ __forceinline__ double tmin(double a, double b) { return fmin(a, b); 
 __device__ __forceinline__ double tmax(double a, double b) { return fmax(a, b); }
 
 // 4 consecutive values from shared memory (broadcast read: all lanes, same address).
+// 16-byte shared-memory load from a 32-bit shared-window address (computed once per
+// tile, so the loop does not re-derive the window base every iteration).
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ float4 lds128(uint32_t a)
+{
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+
 template <typename T> struct Vec4 { T v[4]; };
 
 __device__ __forceinline__ Vec4<float> lds4(const float *p)

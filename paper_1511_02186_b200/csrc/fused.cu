@@ -53,8 +53,8 @@ __global__ void __launch_bounds__(kBlock) fused_fixed_kernel(const FusedArgs a)
             bulk_g2s(d, a.f.cx + off, B, &ring.full[slot]);
             bulk_g2s(d + TILE, a.f.cy + off, B, &ring.full[slot]);
             bulk_g2s(d + 2 * TILE, a.f.pp + off, B, &ring.full[slot]);
-            bulk_g2s(d + 3 * TILE, a.px + off, B, &ring.full[slot]);
-            bulk_g2s(d + 4 * TILE, a.py + off, B, &ring.full[slot]);
+            bulk_g2s(d + 3 * TILE, a.f.px + off, B, &ring.full[slot]);
+            bulk_g2s(d + 4 * TILE, a.f.py + off, B, &ring.full[slot]);
         } else {
             const int64_t off = (int64_t)(gt - nt) * TILE;
             mbar_arrive_expect_tx(&ring.full[slot], 3u * B);
@@ -158,7 +158,8 @@ int launch_fused_fixed(const void *data, int64_t ndp, int64_t nd, const FilterDa
     a.pz = p + 2 * ndp;
     a.ndp = ndp;
     a.nd = nd;
-    a.f = FilterArgs{c, c + ndp, c + 2 * ndp, filt->c_x, filt->c_y, filt->r1};
+    a.f = FilterArgs{c, c + ndp, c + 2 * ndp, p, p + ndp, filt->c_x, filt->c_y, filt->r1, filt->cell_start,
+                     filt->grid};  // caller's order
     a.qx = (const float *)qx;
     a.qy = (const float *)qy;
     a.nq = nq;

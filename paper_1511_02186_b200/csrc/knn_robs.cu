@@ -37,7 +37,14 @@ template <typename T> struct KnnArgs {
     Scratch *sc;
     int dists_sq;  // 1: dists receives the k squared distances s (data-sharded partial lists)
     T *lists;      // split mode (gridDim.y = S > 1): per-split k smallest s, [S][nq][k] ascending
+    const int *perm;  // nullable: launch slot i evaluates query perm[i] (spatial order, §4.7)
 };
+
+// Query index of launch slot `pos` (identity without a permutation).
+template <typename T> __device__ __forceinline__ int64_t query_of(const KnnArgs<T> &a, int64_t pos)
+{
+    return (a.perm && pos < a.nq) ? (int64_t)a.perm[pos] : pos;
+}
 
 // Split mode: this CTA scans data tiles [t0, t0 + nloc) (blockIdx.y of gridDim.y equal
 // ranges); S = 1 covers everything.
@@ -54,11 +61,11 @@ __device__ __forceinline__ TileRange split_range(int ntiles)
 // Split-mode epilogue: the CTA's ascending k smallest squared distances per query.
 template <typename T, int K, int Q>
 __device__ __forceinline__ void knn_write_split(const KnnArgs<T> &a, T (&buf)[Q][K], const bool (&valid)[Q],
-                                                int64_t base, int k0)
+                                                const int64_t (&qid)[Q], int k0)
 {
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        const int64_t idx = base + q * kBlock;
+        const int64_t idx = qid[q];
         if (!valid[q]) continue;
         T *o = a.lists + ((int64_t)blockIdx.y * a.nq + idx) * a.k;
 #pragma unroll
@@ -97,13 +104,15 @@ __device__ __forceinline__ void warp_minmax(double v, bool valid, unsigned long 
 // Query loads for the Q queries of this thread (strided by the block for coalescing),
 // with the non-finite check (smallest failing index -> scratch).
 template <typename T, int Q>
-__device__ __forceinline__ void load_queries(const T *qxp, const T *qyp, int64_t nq, int64_t base, Scratch *sc,
-                                             T (&qx)[Q], T (&qy)[Q], bool (&valid)[Q])
+__device__ __forceinline__ void load_queries(const KnnArgs<T> &a, int64_t base, T (&qx)[Q], T (&qy)[Q],
+                                             bool (&valid)[Q], int64_t (&qid)[Q])
 {
+    const T *qxp = a.qx, *qyp = a.qy;
+    Scratch *sc = a.sc;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        const int64_t idx = base + q * kBlock;
-        valid[q] = idx < nq;
+        valid[q] = base + q * kBlock < a.nq;
+        const int64_t idx = qid[q] = query_of(a, base + q * kBlock);
         qx[q] = valid[q] ? qxp[idx] : T(0);
         qy[q] = valid[q] ? qyp[idx] : T(0);
         if (valid[q] && !(isfinite(qx[q]) && isfinite(qy[q]))) atomicMin(&sc->err_idx, (long long)idx);
@@ -115,7 +124,7 @@ __device__ __forceinline__ void load_queries(const T *qxp, const T *qyp, int64_t
 // resets the scratch).  Must be reached by all threads.
 template <typename T, int K, int Q>
 __device__ __forceinline__ void knn_epilogue(const KnnArgs<T> &a, T (&buf)[Q][K], const bool (&valid)[Q],
-                                             int64_t base, int k0)
+                                             const int64_t (&qid)[Q], int k0)
 {
     const int tid = threadIdx.x, lane = tid & 31;
     T robs_l[Q];
@@ -124,7 +133,7 @@ __device__ __forceinline__ void knn_epilogue(const KnnArgs<T> &a, T (&buf)[Q][K]
         T robs, d1;
         robs_of<T, K>(buf[q], k0, a.k, robs, d1);
         robs_l[q] = robs;
-        const int64_t idx = base + q * kBlock;
+        const int64_t idx = qid[q];
         if (valid[q]) {
             if (a.r_obs) a.r_obs[idx] = robs;
             if (a.d1sq) a.d1sq[idx] = d1;
@@ -199,7 +208,8 @@ __global__ void __launch_bounds__(kBlock) knn_robs_kernel(const KnnArgs<T> a)
     const int64_t base = (int64_t)blockIdx.x * (kBlock * Q) + threadIdx.x;
     T qx[Q], qy[Q];
     bool valid[Q];
-    load_queries<T, Q>(a.qx, a.qy, a.nq, base, a.sc, qx, qy, valid);
+    int64_t qid[Q];
+    load_queries<T, Q>(a, base, qx, qy, valid, qid);
 
     // register top-K; slots [0, K-k) hold -inf sentinels (never displaced)
     T buf[Q][K];
@@ -240,9 +250,9 @@ __global__ void __launch_bounds__(kBlock) knn_robs_kernel(const KnnArgs<T> a)
         ring.release(t, ntiles, issue);
     }
     if constexpr (SPLIT)
-        knn_write_split<T, K, Q>(a, buf, valid, base, k0);
+        knn_write_split<T, K, Q>(a, buf, valid, qid, k0);
     else
-        knn_epilogue<T, K, Q>(a, buf, valid, base, k0);
+        knn_epilogue<T, K, Q>(a, buf, valid, qid, k0);
 }
 
 // ---------------------------------------------------------------------------------
@@ -259,20 +269,33 @@ __global__ void __launch_bounds__(kBlock) knn_filter_kernel(const KnnArgs<float>
     float *spy = spx + STAGES * TILE;
     Ring<STAGES> ring{reinterpret_cast<uint64_t *>(spy + STAGES * TILE),
                       reinterpret_cast<uint64_t *>(spy + STAGES * TILE) + STAGES};
-    const TileRange tr = SPLIT ? split_range((int)(a.ndp / TILE)) : TileRange{0, (int)(a.ndp / TILE)};
+    const int nt_all = (int)(a.ndp / TILE);
+    const TileRange tr = SPLIT ? split_range(nt_all) : TileRange{0, nt_all};
     const int ntiles = tr.nloc;
+    // Spatial order (§4.7): the CTA's queries are neighbours, so it starts its scan at the
+    // (Morton-sorted) data tile under its middle query and wraps around -- the top-k is
+    // near-final after the first tiles and the filter then rejects almost every group.
+    int start = 0;
+    if (!SPLIT && a.perm) {
+        const int64_t mid = min((int64_t)blockIdx.x * (kBlock * Q) + kBlock * Q / 2, a.nq - 1);
+        const int64_t qm = a.perm[mid];
+        start = f.cell_start[morton_cell(a.qx[qm], a.qy[qm], f.grid)] / TILE - 1;
+        start = start < 0 ? start + nt_all : (start >= nt_all ? nt_all - 1 : start);
+    }
     if (threadIdx.x == 0) ring.init();
     __syncthreads();
 
     auto issue = [&](int tile, int slot) {
         constexpr uint32_t B = TILE * sizeof(float);
         mbar_arrive_expect_tx(&ring.full[slot], 5u * B);
-        const int64_t off = (int64_t)(tr.t0 + tile) * TILE;
+        int pt = tr.t0 + tile + start;
+        pt = pt >= nt_all ? pt - nt_all : pt;
+        const int64_t off = (int64_t)pt * TILE;
         bulk_g2s(scx + slot * TILE, f.cx + off, B, &ring.full[slot]);
         bulk_g2s(scy + slot * TILE, f.cy + off, B, &ring.full[slot]);
         bulk_g2s(spp + slot * TILE, f.pp + off, B, &ring.full[slot]);
-        bulk_g2s(spx + slot * TILE, a.px + off, B, &ring.full[slot]);
-        bulk_g2s(spy + slot * TILE, a.py + off, B, &ring.full[slot]);
+        bulk_g2s(spx + slot * TILE, f.px + off, B, &ring.full[slot]);
+        bulk_g2s(spy + slot * TILE, f.py + off, B, &ring.full[slot]);
     };
     if (threadIdx.x == 0)
         for (int s = 0; s < STAGES && s < ntiles; ++s) issue(s, s);
@@ -280,7 +303,8 @@ __global__ void __launch_bounds__(kBlock) knn_filter_kernel(const KnnArgs<float>
     const int64_t base = (int64_t)blockIdx.x * (kBlock * Q) + threadIdx.x;
     float qx[Q], qy[Q];
     bool valid[Q];
-    load_queries<float, Q>(a.qx, a.qy, a.nq, base, a.sc, qx, qy, valid);
+    int64_t qid[Q];
+    load_queries<float, Q>(a, base, qx, qy, valid, qid);
     const int k0 = K - a.k;
     KnnF32State<K, Q> st;
 #pragma unroll
@@ -293,9 +317,9 @@ __global__ void __launch_bounds__(kBlock) knn_filter_kernel(const KnnArgs<float>
         ring.release(t, ntiles, issue);
     }
     if constexpr (SPLIT)
-        knn_write_split<float, K, Q>(a, st.buf, valid, base, k0);
+        knn_write_split<float, K, Q>(a, st.buf, valid, qid, k0);
     else
-        knn_epilogue<float, K, Q>(a, st.buf, valid, base, k0);
+        knn_epilogue<float, K, Q>(a, st.buf, valid, qid, k0);
 }
 
 // ---------------------------------------------------------------------------------
@@ -333,8 +357,18 @@ template <int K, int Q, int G, bool SPLIT> static int set_filter_attrs(size_t sm
                : -1;
 }
 
+// Query batches at least this large are spatially ordered first;
+// AIDW_KNN_ORDER=0 disables (tests compare both).
+static bool order_queries(int64_t nq)
+{
+    constexpr int64_t kOrderMinQ = 32768;
+    const char *e = getenv("AIDW_KNN_ORDER");
+    return nq >= kOrderMinQ && !(e && e[0] == '0');
+}
+
 template <int K, int Q, int G = 8>
-static int launch_knn_filter_t(KnnArgs<float> a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp)
+static int launch_knn_filter_t(KnnArgs<float> a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp,
+                               FilterData *fd)
 {
     const size_t smem = (size_t)5 * kStagesKF * kTileKF * sizeof(float) + 2 * kStagesKF * sizeof(uint64_t);
     if (set_filter_attrs<K, Q, G, false>(smem) < 0) return -1;
@@ -342,13 +376,28 @@ static int launch_knn_filter_t(KnnArgs<float> a, const FilterArgs &f, cudaStream
     const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
     const int S =
         knn_split_factor((const void *)knn_filter_kernel<K, Q, G, false>, smem, grid, (int)(a.ndp / kTileKF), a, sp);
+    int pre = 0;
     if (S == 1) {
-        knn_filter_kernel<K, Q, G, false><<<grid, kBlock, smem, st>>>(a, f);
+        FilterArgs fo = f;
+        if (fd && fd->cell_start && order_queries(a.nq)) {
+            pre = launch_order_queries(a.qx, a.qy, a.nq, fd, &fd->qorder, &a.perm, st);
+            if (pre < 0) return -1;
+            if (a.perm) {  // Morton-ordered copy of the data
+                const float *c = static_cast<const float *>(fd->arrays);
+                fo.cx = c + 3 * a.ndp;
+                fo.cy = c + 4 * a.ndp;
+                fo.pp = c + 5 * a.ndp;
+                fo.px = c + 6 * a.ndp;
+                fo.py = c + 7 * a.ndp;
+            }
+        }
+        knn_filter_kernel<K, Q, G, false><<<grid, kBlock, smem, st>>>(a, fo);
     } else {
         if (set_filter_attrs<K, Q, G, true>(smem) < 0) return -1;
         knn_filter_kernel<K, Q, G, true><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, f);
     }
-    return knn_finish(a, S, st);
+    const int n = knn_finish(a, S, st);
+    return n < 0 ? -1 : n + pre;
 }
 
 static int knn_variant()
@@ -361,31 +410,32 @@ static int knn_variant()
     return v;
 }
 
-static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp)
+static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp,
+                             FilterData *fd)
 {
     const int k = a.k;
     if (k <= 10 && k > 8) {
         switch (knn_variant()) {  // tuning sweep (tools/tune_knn.py)
-        case 2: return launch_knn_filter_t<10, 4, 8>(a, f, st, sp);
-        case 3: return launch_knn_filter_t<10, 2, 16>(a, f, st, sp);
-        case 4: return launch_knn_filter_t<10, 2, 8>(a, f, st, sp);
-        case 5: return launch_knn_filter_t<10, 3, 16>(a, f, st, sp);
-        case 6: return launch_knn_filter_t<10, 4, 16>(a, f, st, sp);
-        case 7: return launch_knn_filter_t<10, 2, 32>(a, f, st, sp);
+        case 2: return launch_knn_filter_t<10, 4, 8>(a, f, st, sp, fd);
+        case 3: return launch_knn_filter_t<10, 2, 16>(a, f, st, sp, fd);
+        case 4: return launch_knn_filter_t<10, 2, 8>(a, f, st, sp, fd);
+        case 5: return launch_knn_filter_t<10, 3, 16>(a, f, st, sp, fd);
+        case 6: return launch_knn_filter_t<10, 4, 16>(a, f, st, sp, fd);
+        case 7: return launch_knn_filter_t<10, 2, 32>(a, f, st, sp, fd);
         default: break;
         }
     }
     // Q = 2 queries per thread, G = 16 points per warp vote (best measured, r01)
-    if (k <= 1) return launch_knn_filter_t<1, 2, 16>(a, f, st, sp);
-    if (k <= 2) return launch_knn_filter_t<2, 2, 16>(a, f, st, sp);
-    if (k <= 4) return launch_knn_filter_t<4, 2, 16>(a, f, st, sp);
-    if (k <= 8) return launch_knn_filter_t<8, 2, 16>(a, f, st, sp);
-    if (k <= 10) return launch_knn_filter_t<10, 2, 16>(a, f, st, sp);
-    if (k <= 12) return launch_knn_filter_t<12, 2, 16>(a, f, st, sp);
-    if (k <= 15) return launch_knn_filter_t<15, 2, 16>(a, f, st, sp);
-    if (k <= 16) return launch_knn_filter_t<16, 2, 16>(a, f, st, sp);
-    if (k <= 24) return launch_knn_filter_t<24, 2>(a, f, st, sp);
-    return launch_knn_filter_t<32, 2>(a, f, st, sp);
+    if (k <= 1) return launch_knn_filter_t<1, 2, 16>(a, f, st, sp, fd);
+    if (k <= 2) return launch_knn_filter_t<2, 2, 16>(a, f, st, sp, fd);
+    if (k <= 4) return launch_knn_filter_t<4, 2, 16>(a, f, st, sp, fd);
+    if (k <= 8) return launch_knn_filter_t<8, 2, 16>(a, f, st, sp, fd);
+    if (k <= 10) return launch_knn_filter_t<10, 2, 16>(a, f, st, sp, fd);
+    if (k <= 12) return launch_knn_filter_t<12, 2, 16>(a, f, st, sp, fd);
+    if (k <= 15) return launch_knn_filter_t<15, 2, 16>(a, f, st, sp, fd);
+    if (k <= 16) return launch_knn_filter_t<16, 2, 16>(a, f, st, sp, fd);
+    if (k <= 24) return launch_knn_filter_t<24, 2>(a, f, st, sp, fd);
+    return launch_knn_filter_t<32, 2>(a, f, st, sp, fd);
 }
 
 // ---------------------------------------------------------------------------------
@@ -411,7 +461,8 @@ __global__ void __launch_bounds__(kBlock) knn_merge_kernel(const KnnArgs<T> a, c
                 if (s < buf[0][K - 1]) topk_insert<T, K>(buf[0], s);
             }
         }
-    knn_epilogue<T, K, Q>(a, buf, valid, base, k0);
+    const int64_t qid[Q] = {base};
+    knn_epilogue<T, K, Q>(a, buf, valid, qid, k0);
 }
 
 template <typename T, int K>
@@ -443,11 +494,11 @@ int launch_knn_merge(int dtype, int k, const void *lists, int P, int64_t nq, voi
 {
     if (dtype == 0) {
         KnnArgs<float> a{nullptr, nullptr, 0, nullptr, nullptr, nq, k, (float *)r_obs, (float *)d1sq,
-                         (float *)minmax, nullptr, sc, 0, nullptr};
+                         (float *)minmax, nullptr, sc, 0, nullptr, nullptr};
         return dispatch_merge(a, (const float *)lists, P, st);
     }
     KnnArgs<double> a{nullptr, nullptr, 0, nullptr, nullptr, nq, k, (double *)r_obs, (double *)d1sq,
-                      (double *)minmax, nullptr, sc, 0, nullptr};
+                      (double *)minmax, nullptr, sc, 0, nullptr, nullptr};
     return dispatch_merge(a, (const double *)lists, P, st);
 }
 
@@ -497,22 +548,25 @@ static int dispatch_k(const KnnArgs<T> &a, cudaStream_t st, SplitBuf *sp)
 
 int launch_knn(int dtype, int k, const void *data, int64_t ndp, const void *qx, const void *qy,
                int64_t nq, void *r_obs, void *d1sq, void *minmax, void *dists, Scratch *sc,
-               const FilterData *filt, cudaStream_t st, int dists_sq, SplitBuf *sp)
+               FilterData *filt, cudaStream_t st, int dists_sq, SplitBuf *sp)
 {
     if (dtype == 0) {
         const float *p = static_cast<const float *>(data);
         KnnArgs<float> a{p, p + ndp, ndp, (const float *)qx, (const float *)qy, nq, k,
-                         (float *)r_obs, (float *)d1sq, (float *)minmax, (float *)dists, sc, dists_sq, nullptr};
+                         (float *)r_obs, (float *)d1sq, (float *)minmax, (float *)dists, sc, dists_sq, nullptr, nullptr};
         if (filt && filt->arrays) {
             const float *c = static_cast<const float *>(filt->arrays);
-            FilterArgs f{c, c + ndp, c + 2 * ndp, filt->c_x, filt->c_y, filt->r1};
-            return dispatch_filter_k(a, f, st, sp);
+            // caller's order (unordered launches); the Morton-ordered copy is selected in
+            // launch_knn_filter_t when the query batch is ordered (§4.7)
+            FilterArgs f{c, c + ndp, c + 2 * ndp, p, p + ndp, filt->c_x, filt->c_y, filt->r1, filt->cell_start,
+                         filt->grid};
+            return dispatch_filter_k(a, f, st, sp, filt);
         }
         return dispatch_k(a, st, sp);
     }
     const double *p = static_cast<const double *>(data);
     KnnArgs<double> a{p, p + ndp, ndp, (const double *)qx, (const double *)qy, nq, k,
-                      (double *)r_obs, (double *)d1sq, (double *)minmax, (double *)dists, sc, dists_sq, nullptr};
+                      (double *)r_obs, (double *)d1sq, (double *)minmax, (double *)dists, sc, dists_sq, nullptr, nullptr};
     return dispatch_k(a, st, sp);
 }
 

@@ -1,0 +1,140 @@
+// order.cu -- spatial (Morton) order for the fp32 kNN pass.
+//
+// The brute-force kNN (every pair evaluated) does not depend on the
+// order in which data points are visited or queries are assigned to threads: the k
+// smallest distances are a multiset.  Its COST does: a point that enters a query's
+// top-k costs an insertion, and with random orders every warp keeps meeting points
+// that are near one of its 64 queries.  So
+//  * a second copy of the kNN filter data is counting-sorted by Morton cell at handle
+//    creation (the weighting pass, and kNN launches without a query order -- small or
+//    split batches, for which a sorted scan would insert far more -- keep the caller's
+//    order);
+//  * each large query batch is counting-sorted the same way into a permutation, so a
+//    CTA's 256 queries are neighbours;
+//  * the kNN CTA starts its scan at the sorted data under its queries and wraps around.
+// Order within a cell follows atomics and may differ between runs; no result depends on
+// it.  Each sort is three kernels: cell histogram, single-CTA exclusive scan, scatter.
+#include "passes.cuh"
+
+namespace aidw {
+
+namespace {
+
+__global__ void cell_hist_kernel(const float *__restrict__ x, const float *__restrict__ y, int64_t n, OrderGrid g,
+                                 unsigned *__restrict__ counts)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&counts[morton_cell(x[i], y[i], g)], 1u);
+}
+
+// Exclusive scan of kCells counts by one CTA of 1024 threads (64 cells per thread);
+// writes start[0..kCells] (start[kCells] = total) and a cursor copy for the scatter.
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads) cell_scan_kernel(const unsigned *__restrict__ counts,
+                                                                 int *__restrict__ start, int *__restrict__ cursor)
+{
+    constexpr int per = kCells / kScanThreads;
+    __shared__ unsigned part[kScanThreads];
+    const int t = threadIdx.x;
+    unsigned sum = 0;
+    for (int i = 0; i < per; ++i) sum += counts[t * per + i];
+    part[t] = sum;
+    __syncthreads();
+    for (int o = 1; o < kScanThreads; o <<= 1) {  // Hillis-Steele inclusive scan
+        const unsigned v = t >= o ? part[t - o] : 0u;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    unsigned run = part[t] - sum;
+    for (int i = 0; i < per; ++i) {
+        const int c = t * per + i;
+        start[c] = (int)run;
+        if (cursor) cursor[c] = (int)run;
+        run += counts[c];
+    }
+    if (t == kScanThreads - 1) start[kCells] = (int)run;
+}
+
+// Data: the centred filter values in the caller's order (for unordered launches) and,
+// with the coordinates, at sorted positions; padding slots [nd, ndp) get +inf.
+__global__ void order_data_scatter_kernel(const float *__restrict__ px, const float *__restrict__ py, int64_t nd,
+                                          int64_t ndp, OrderGrid g, float c_x, float c_y,
+                                          int *__restrict__ cursor, float *__restrict__ out)
+{
+    float *ux = out, *uy = out + ndp, *up = out + 2 * ndp;  // caller's order
+    float *cx = out + 3 * ndp, *cy = out + 4 * ndp, *pp = out + 5 * ndp, *sx = out + 6 * ndp, *sy = out + 7 * ndp;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndp;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < nd) {
+            const float x = px[i], y = py[i];
+            const int64_t o = atomicAdd(&cursor[morton_cell(x, y, g)], 1);
+            const float a = __fsub_rn(x, c_x), b = __fsub_rn(y, c_y);
+            const float p2 = __fmaf_rn(a, a, __fmul_rn(b, b));
+            ux[i] = cx[o] = a;
+            uy[i] = cy[o] = b;
+            up[i] = pp[o] = p2;
+            sx[o] = x;
+            sy[o] = y;
+        } else {
+            ux[i] = uy[i] = up[i] = cx[i] = cy[i] = pp[i] = sx[i] = sy[i] = pos_inf<float>();
+        }
+    }
+}
+
+__global__ void order_query_scatter_kernel(const float *__restrict__ qx, const float *__restrict__ qy, int64_t nq,
+                                           OrderGrid g, int *__restrict__ cursor, int *__restrict__ perm)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x)
+        perm[atomicAdd(&cursor[morton_cell(qx[i], qy[i], g)], 1)] = (int)i;
+}
+
+unsigned grid_for(int64_t n)
+{
+    int64_t b = (n + 255) / 256;
+    if (b > 148 * 8) b = 148 * 8;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+int launch_order_data(const void *data, int64_t ndp, int64_t nd, FilterData *fd, cudaStream_t st)
+{
+    const float *px = static_cast<const float *>(data), *py = px + ndp;
+    unsigned *counts = nullptr;
+    int *cursor = nullptr;
+    if (cudaMallocAsync(&counts, kCells * sizeof(unsigned), st) != cudaSuccess ||
+        cudaMallocAsync(&cursor, kCells * sizeof(int), st) != cudaSuccess ||
+        cudaMemsetAsync(counts, 0, kCells * sizeof(unsigned), st) != cudaSuccess)
+        return -1;
+    cell_hist_kernel<<<grid_for(nd), 256, 0, st>>>(px, py, nd, fd->grid, counts);
+    cell_scan_kernel<<<1, kScanThreads, 0, st>>>(counts, fd->cell_start, cursor);
+    order_data_scatter_kernel<<<grid_for(ndp), 256, 0, st>>>(px, py, nd, ndp, fd->grid, fd->c_x, fd->c_y, cursor,
+                                                             static_cast<float *>(fd->arrays));
+    const bool ok = cudaPeekAtLastError() == cudaSuccess;
+    cudaFreeAsync(counts, st);
+    cudaFreeAsync(cursor, st);
+    return ok ? 3 : -1;
+}
+
+int launch_order_queries(const float *qx, const float *qy, int64_t nq, const FilterData *fd, SplitBuf *buf,
+                         const int **perm, cudaStream_t st)
+{
+    // buf layout: counts [kCells] | start [kCells + 1] | cursor [kCells] | perm [nq]
+    const size_t head = (size_t)(3 * kCells + 1) * sizeof(int);
+    char *b = static_cast<char *>(buf->reserve(head + (size_t)nq * sizeof(int)));
+    if (!b) return 0;  // no memory: run unordered
+    unsigned *counts = reinterpret_cast<unsigned *>(b);
+    int *start = reinterpret_cast<int *>(b) + kCells;
+    int *cursor = start + kCells + 1;
+    int *p = cursor + kCells;
+    if (cudaMemsetAsync(counts, 0, kCells * sizeof(unsigned), st) != cudaSuccess) return -1;
+    cell_hist_kernel<<<grid_for(nq), 256, 0, st>>>(qx, qy, nq, fd->grid, counts);
+    cell_scan_kernel<<<1, kScanThreads, 0, st>>>(counts, start, cursor);
+    order_query_scatter_kernel<<<grid_for(nq), 256, 0, st>>>(qx, qy, nq, fd->grid, cursor, p);
+    if (cudaPeekAtLastError() != cudaSuccess) return -1;
+    *perm = p;
+    return 3;
+}
+
+}  // namespace aidw

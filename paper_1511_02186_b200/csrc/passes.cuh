@@ -88,9 +88,12 @@ __device__ __forceinline__ void robs_of(const T (&b)[K], int k0, int k, T &robs,
 //   most 2u (n1 + R1).  Hence s < thr  =>  t~ < (sqrt(thr)(1+4u) + 4u(n1+R1))^2 - |q'|^2
 //   + 8u(n1+R1)^2; the constants below double every term.
 struct FilterArgs {
-    const float *cx, *cy, *pp;  // centred filter arrays, padded with +inf
+    const float *cx, *cy, *pp;  // centred filter arrays, padded with +inf (spatial order)
+    const float *px, *py;       // the same points' coordinates (canonical re-check)
     float c_x, c_y;             // centre
     float r1;                   // R1 bound
+    const int *cell_start;      // first sorted position of each Morton cell (§4.7)
+    OrderGrid grid;
 };
 
 // thr_of: the filter threshold for the canonical k-th distance thr, in fp32 with every
@@ -117,8 +120,8 @@ struct KnnF32State {
         qx[q] = x;
         qy[q] = y;
         const float qcx = __fsub_rn(x, f.c_x), qcy = __fsub_rn(y, f.c_y);
-        A[q] = -2.0f * qcx;
-        B[q] = -2.0f * qcy;
+        A[q] = opaque(-2.0f * qcx);  // opaque: keep in a register, never re-derived per group
+        B[q] = opaque(-2.0f * qcy);
         thr[q] = pos_inf<float>();
         const double u = 0x1p-24;
         const double qq = (double)qcx * (double)qcx + (double)qcy * (double)qcy;
@@ -131,52 +134,75 @@ struct KnnF32State {
     }
 };
 
-// One smem tile of TILE points: filter values in groups of G points per warp vote
-// (loaded in chunks of 8 points, so only one chunk's inputs are live at a time); a
-// bitmask rare path re-checks only the passing pairs with the canonical distance.
+// Filter values t = pp + A cx + B cy of the 8 points at tile offset j for query q, as
+// four packed couples (2 FFMA2 each).
+template <int K, int Q>
+__device__ __forceinline__ void filter8(const KnnF32State<K, Q> &st, int q, const float *__restrict__ tcx,
+                                        const float *__restrict__ tcy, const float *__restrict__ tpp, int j,
+                                        float (&t)[8])
+{
+#pragma unroll
+    for (int g = 0; g < 8; g += 4) {
+        const float4 CX = *reinterpret_cast<const float4 *>(tcx + j + g);
+        const float4 CY = *reinterpret_cast<const float4 *>(tcy + j + g);
+        const float4 PP = *reinterpret_cast<const float4 *>(tpp + j + g);
+        const f32x2 a = fma2(splat2(st.B[q]), pack2(CY.x, CY.y), fma2(splat2(st.A[q]), pack2(CX.x, CX.y), pack2(PP.x, PP.y)));
+        const f32x2 b = fma2(splat2(st.B[q]), pack2(CY.z, CY.w), fma2(splat2(st.A[q]), pack2(CX.z, CX.w), pack2(PP.z, PP.w)));
+        t[g] = a.x;
+        t[g + 1] = a.y;
+        t[g + 2] = b.x;
+        t[g + 3] = b.y;
+    }
+}
+
+// One smem tile of TILE points in groups of G points per warp vote.  The main loop keeps
+// only a running 3-input-min per query (chunks of 8 points: 8 FFMA2 + 4 FMNMX3 per query,
+// the smem loads shared by the Q queries); a group that passes for some lane re-derives
+// its t values in the rare path, builds the bitmask of passing pairs and re-checks only
+// those with the canonical distance.
 template <int K, int Q, int G, int TILE>
 __device__ __forceinline__ void knn_f32_tile(KnnF32State<K, Q> &st, const float *__restrict__ tcx,
                                              const float *__restrict__ tcy, const float *__restrict__ tpp,
                                              const float *__restrict__ tpx, const float *__restrict__ tpy)
 {
     static_assert(G % 8 == 0 && G <= 32 && TILE % G == 0, "group size");
+    const uint32_t acx = smem_addr(tcx), acy = smem_addr(tcy), app = smem_addr(tpp);
 #pragma unroll 1
     for (int j = 0; j < TILE; j += G) {
-        float tv[Q][G];
+        float mn[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) mn[q] = pos_inf<float>();
 #pragma unroll
         for (int c = 0; c < G; c += 8) {
             float cxv[8], cyv[8], ppv[8];
 #pragma unroll
             for (int g = 0; g < 8; g += 4) {
-                const float4 CX = *reinterpret_cast<const float4 *>(tcx + j + c + g);
-                const float4 CY = *reinterpret_cast<const float4 *>(tcy + j + c + g);
-                const float4 PP = *reinterpret_cast<const float4 *>(tpp + j + c + g);
+                const uint32_t o = (uint32_t)(j + c + g) * 4u;
+                const float4 CX = lds128(acx + o);
+                const float4 CY = lds128(acy + o);
+                const float4 PP = lds128(app + o);
                 cxv[g] = CX.x; cxv[g + 1] = CX.y; cxv[g + 2] = CX.z; cxv[g + 3] = CX.w;
                 cyv[g] = CY.x; cyv[g + 1] = CY.y; cyv[g + 2] = CY.z; cyv[g + 3] = CY.w;
                 ppv[g] = PP.x; ppv[g + 1] = PP.y; ppv[g + 2] = PP.z; ppv[g + 3] = PP.w;
             }
 #pragma unroll
-            for (int q = 0; q < Q; ++q)
+            for (int q = 0; q < Q; ++q) {
+                float t[8];
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
                     const f32x2 tt = fma2(splat2(st.B[q]), pack2(cyv[2 * h], cyv[2 * h + 1]),
                                           fma2(splat2(st.A[q]), pack2(cxv[2 * h], cxv[2 * h + 1]),
                                                pack2(ppv[2 * h], ppv[2 * h + 1])));
-                    tv[q][c + 2 * h] = tt.x;
-                    tv[q][c + 2 * h + 1] = tt.y;
+                    t[2 * h] = tt.x;
+                    t[2 * h + 1] = tt.y;
                 }
+                mn[q] = fmin3(fmin3(t[0], t[1], t[2]), fmin3(t[3], t[4], t[5]), fmin3(t[6], t[7], mn[q]));
+            }
         }
         bool hq[Q], hit = false;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            float m[G];
-#pragma unroll
-            for (int i = 0; i < G; ++i) m[i] = tv[q][i];
-#pragma unroll
-            for (int w = 1; w < G; w *= 2)
-#pragma unroll
-                for (int i = 0; i + w < G; i += 2 * w) m[i] = fminf(m[i], m[i + w]);
-            hq[q] = m[0] <= st.thr[q];
+            hq[q] = mn[q] <= st.thr[q];
             hit |= hq[q];
         }
         if (__any_sync(0xffffffffu, hit)) {
@@ -186,7 +212,12 @@ __device__ __forceinline__ void knn_f32_tile(KnnF32State<K, Q> &st, const float 
                 unsigned mask = 0;
                 if (hq[q]) {
 #pragma unroll
-                    for (int e = 0; e < G; ++e) mask |= (tv[q][e] <= st.thr[q]) ? (1u << e) : 0u;
+                    for (int c = 0; c < G; c += 8) {
+                        float t[8];
+                        filter8(st, q, tcx, tcy, tpp, j + c, t);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) mask |= (t[e] <= st.thr[q]) ? (1u << (c + e)) : 0u;
+                    }
                 }
                 bool inserted = false;
                 while (__any_sync(0xffffffffu, mask != 0)) {

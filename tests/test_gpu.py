@@ -296,6 +296,42 @@ def test_split_bit_identical(P, monkeypatch, dtype, nd, nq, k):
             assert np.array_equal(u, v, equal_nan=True), (sv, n)
 
 
+@pytest.mark.parametrize("case", ["C3", "outside", "duplicates"])
+def test_knn_order_bit_identical(P, orc, monkeypatch, case):
+    """Spatial order (Morton-sorted data copy, query permutation, per-CTA
+    start tile) changes only the visiting order of the brute-force kNN: lists, r_obs,
+    d1sq, bounds and Z are bit-identical to the unordered launch, and exact vs the
+    oracle's float instantiation on sampled queries."""
+    if case == "C3":
+        x, y, z = datagen.make_data("C3")
+        qx, qy = datagen.make_queries("C3")
+        k = 15
+    else:
+        x, y, z, qx, qy = datagen.random_cloud(77, 60000, 40000)
+        k = 10
+        if case == "outside":  # queries beyond the data bbox (clamped to border cells) + a NaN-free far field
+            qx = qx * 2.0 - 0.5  # exact in fp32 (2^-23 grid)
+            qy = qy * 2.0 - 0.5
+        else:  # many coincident data points and queries on data points
+            x[1::3], y[1::3] = x[::3][: len(x[1::3])], y[::3][: len(y[1::3])]
+            qx[::5], qy[::5] = x[: len(qx[::5])], y[: len(qy[::5])]
+    eng = P.AIDW(x, y, z)
+    res = {}
+    for sv in ("0", None):
+        if sv is None:
+            monkeypatch.delenv("AIDW_KNN_ORDER", raising=False)
+        else:
+            monkeypatch.setenv("AIDW_KNN_ORDER", sv)
+        r, d1, mm, dd = eng.knn_robs(qx, qy, k, want_dists=True)
+        zr = eng.run(qx, qy, k, LV, P.GLOBAL)
+        res[sv] = [t.cpu().numpy() for t in (r, d1, mm, dd, zr)]
+    for n, (u, v) in enumerate(zip(res[None], res["0"])):
+        assert np.array_equal(u, v), n
+    idx = np.random.default_rng(5).choice(len(qx), 300, replace=False)
+    ro = orc.knn_f32(x, y, qx[idx], qy[idx], k)
+    assert np.array_equal(res[None][0][idx], ro)
+
+
 def test_errors(P):
     x, y, z, qx, qy = datagen.random_cloud(1, 100, 10)
     with pytest.raises(P.AidwError, match="DEGENERATE"):

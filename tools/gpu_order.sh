@@ -1,0 +1,21 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout 900 -rA > gpurun_out/pytest_gpu.log 2>&1
+timeout 300 python tools/configs_bench.py --configs C2,C3,C4 > gpurun_out/configs.jsonl 2>&1
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+KERNELS=knn_filter_kernel bash tools/gpu_ncu.sh ord > /dev/null 2>&1
+tail -3 gpurun_out/smoke.log
+grep -E "FAIL|Error|error" gpurun_out/pytest_gpu.log | head -20
+tail -3 gpurun_out/pytest_gpu.log
+python - <<'P'
+import json
+for fn in ("gpurun_out/configs.jsonl",):
+    print(fn)
+    for l in open(fn):
+        try: r=json.loads(l)
+        except Exception: print(l.strip()); continue
+        print(r["config"], r["dtype"], "knn %.3f alpha %.3f interp %.3f total %.3f ms" % (r["knn_ms"], r["alpha_ms"], r["interp_ms"], r["total_ms"]))
+P
+cut -c1-300 gpurun_out/bench.json
+python tools/ncu_summary.py gpurun_out/ord_knn_filter_kernel.ncu-rep --json gpurun_out/ord_knn.json | head -60
