@@ -422,6 +422,8 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
         case 5: return launch_knn_filter_t<10, 3, 16>(a, f, st, sp, fd);
         case 6: return launch_knn_filter_t<10, 4, 16>(a, f, st, sp, fd);
         case 7: return launch_knn_filter_t<10, 2, 32>(a, f, st, sp, fd);
+        case 8: return launch_knn_filter_t<10, 4, 32>(a, f, st, sp, fd);
+        case 9: return launch_knn_filter_t<10, 3, 32>(a, f, st, sp, fd);
         default: break;
         }
     }
@@ -430,7 +432,10 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
     if (k <= 2) return launch_knn_filter_t<2, 2, 16>(a, f, st, sp, fd);
     if (k <= 4) return launch_knn_filter_t<4, 2, 16>(a, f, st, sp, fd);
     if (k <= 8) return launch_knn_filter_t<8, 2, 16>(a, f, st, sp, fd);
-    if (k <= 10) return launch_knn_filter_t<10, 2, 16>(a, f, st, sp, fd);
+    if (k <= 10) {  // large (spatially ordered) batches: Q = 4, G = 32 (108 vs 115 ms at C4)
+        if (order_queries(a.nq)) return launch_knn_filter_t<10, 4, 32>(a, f, st, sp, fd);
+        return launch_knn_filter_t<10, 2, 16>(a, f, st, sp, fd);
+    }
     if (k <= 12) return launch_knn_filter_t<12, 2, 16>(a, f, st, sp, fd);
     if (k <= 15) return launch_knn_filter_t<15, 2, 16>(a, f, st, sp, fd);
     if (k <= 16) return launch_knn_filter_t<16, 2, 16>(a, f, st, sp, fd);
