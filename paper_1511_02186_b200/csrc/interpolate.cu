@@ -69,21 +69,25 @@ struct XYZRing {
 };
 
 // Generic kernel: fp64 path (and the scalar fp32 variant, AIDW_INTERP_VARIANT=1).
-template <typename T, int Q>
+template <typename T, int Q, bool SPLIT = false>
 __global__ void __launch_bounds__(kBlock) interp_kernel(const InterpArgs<T> a)
 {
     constexpr int TILE = kTileW, STAGES = kStagesW;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ F64Tabs tabs;
     XYZRing<T, TILE, STAGES> r(smem_raw);
-    const int ntiles = (int)(a.ndp / TILE);
+    const int ntiles_all = (int)(a.ndp / TILE);
+    // split mode (gridDim.y = S > 1, §4.6): this CTA covers accumulation blocks [b0, b1)
+    const int nblk = acc_blocks(ntiles_all), S = SPLIT ? (int)gridDim.y : 1;
+    const int b0 = SPLIT ? (int)blockIdx.y * nblk / S : 0, b1 = SPLIT ? ((int)blockIdx.y + 1) * nblk / S : nblk;
+    const int t0 = block_tile(b0, ntiles_all, nblk), ntiles = block_tile(b1, ntiles_all, nblk) - t0;
     if (threadIdx.x == 0) r.ring.init();
     if (sizeof(T) == 8) {
         if (threadIdx.x < 64) tabs.lg[threadIdx.x] = make_double2(kLog2Tab[threadIdx.x][0], kLog2Tab[threadIdx.x][1]);
         if (threadIdx.x < 16) tabs.ex[threadIdx.x] = kExp2Tab[threadIdx.x];
     }
     __syncthreads();
-    auto issue = [&](int tile, int slot) { r.issue(a, tile, slot); };
+    auto issue = [&](int tile, int slot) { r.issue(a, t0 + tile, slot); };
     if (threadIdx.x == 0)
         for (int s = 0; s < STAGES && s < ntiles; ++s) issue(s, s);
 
@@ -105,8 +109,7 @@ __global__ void __launch_bounds__(kBlock) interp_kernel(const InterpArgs<T> a)
         SWZ[q] = 0.0;
     }
 
-    const int nblk = acc_blocks(ntiles);
-    int blk = 0, bend = block_tile(1, ntiles, nblk);
+    int blk = b0, bend = block_tile(b0 + 1, ntiles_all, nblk) - t0;
     double BW[Q], BWZ[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) BW[q] = BWZ[q] = 0.0;
@@ -138,21 +141,27 @@ __global__ void __launch_bounds__(kBlock) interp_kernel(const InterpArgs<T> a)
         if (t + 1 == bend) {  // end of an accumulation block: block sums in block order
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
-                SW[q] += BW[q];
-                SWZ[q] += BWZ[q];
+                if constexpr (SPLIT) {
+                    if (valid[q]) a.bpart[(int64_t)blk * a.nq + base + q * kBlock] = make_double2(BW[q], BWZ[q]);
+                } else {
+                    SW[q] += BW[q];
+                    SWZ[q] += BWZ[q];
+                }
                 BW[q] = BWZ[q] = 0.0;
             }
             ++blk;
-            bend = block_tile(blk + 1, ntiles, nblk);
+            bend = block_tile(blk + 1, ntiles_all, nblk) - t0;
         }
         r.ring.release(t, ntiles, issue);
     }
 
+    if constexpr (!SPLIT) {
 #pragma unroll
-    for (int q = 0; q < Q; ++q)
-        if (valid[q])
-            write_result<T>(a.z, a.partial, base + q * kBlock, SW[q], SWZ[q], d1[q], qx[q], qy[q], a.px, a.py,
-                            a.pz, a.nd);
+        for (int q = 0; q < Q; ++q)
+            if (valid[q])
+                write_result<T>(a.z, a.partial, base + q * kBlock, SW[q], SWZ[q], d1[q], qx[q], qy[q], a.px, a.py,
+                                a.pz, a.nd);
+    }
 }
 
 // Packed fp32 kernel (passes.cuh interp_f32_tile / interp_f32_tile_cls).  With a class
@@ -255,7 +264,7 @@ __global__ void __launch_bounds__(BLOCK, interp_min_blocks(Q) * kBlock / BLOCK)
 
 // Split mode: Z (or the data-sharded partials) from the per-block sums, added in block
 // order exactly as an unsplit launch adds them.
-__global__ void finalize_split_kernel(const InterpArgs<float> a, int nblk)
+template <typename T> __global__ void finalize_split_kernel(const InterpArgs<T> a, int nblk)
 {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.nq; i += (int64_t)gridDim.x * blockDim.x) {
         double SW = 0.0, SWZ = 0.0;
@@ -264,7 +273,7 @@ __global__ void finalize_split_kernel(const InterpArgs<float> a, int nblk)
             SW += v.x;
             SWZ += v.y;
         }
-        write_result<float>(a.z, a.partial, i, SW, SWZ, a.d1sq[i], a.qx[i], a.qy[i], a.px, a.py, a.pz, a.nd);
+        write_result<T>(a.z, a.partial, i, SW, SWZ, a.d1sq[i], a.qx[i], a.qy[i], a.px, a.py, a.pz, a.nd);
     }
 }
 
@@ -311,19 +320,6 @@ __global__ void class_scatter_kernel(const InterpArgs<float> a, unsigned *counts
     }
 }
 
-template <typename T, int Q>
-static int launch_interp_t(const InterpArgs<T> &a, cudaStream_t st)
-{
-    const size_t smem = XYZRing<T, kTileW, kStagesW>::smem_bytes();
-    if (cudaFuncSetAttribute(interp_kernel<T, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return -1;
-    const int64_t per_cta = (int64_t)kBlock * Q;
-    const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
-    interp_kernel<T, Q><<<grid, kBlock, smem, st>>>(a);
-    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
-}
-
 // Split factor for a launch of `grid` CTAs: 1 when the grid already fills `waves`
 // waves of resident CTAs, else enough data splits for ~`waves` waves (<= `maxs`), or
 // `maxs` itself when `full`.  AIDW_SPLIT=0 disables,
@@ -351,6 +347,35 @@ int choose_split(const void *kern, int block, size_t smem, int64_t grid, int max
     if (s < 2) return 1;
     if (full) return maxs;
     return (int)(s < maxs ? s : maxs);
+}
+
+template <typename T, int Q>
+static int launch_interp_t(InterpArgs<T> a, cudaStream_t st, SplitBuf *split = nullptr)
+{
+    const size_t smem = XYZRing<T, kTileW, kStagesW>::smem_bytes();
+    if (cudaFuncSetAttribute(interp_kernel<T, Q, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return -1;
+    const int64_t per_cta = (int64_t)kBlock * Q;
+    const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
+    const int nblk = acc_blocks((int)(a.ndp / kTileW));
+    int S = split ? choose_split((const void *)interp_kernel<T, Q, false>, kBlock, smem, grid, nblk, 16, true) : 1;
+    a.bpart = S > 1 ? static_cast<double2 *>(split->reserve((size_t)nblk * (size_t)a.nq * sizeof(double2)))
+                    : nullptr;
+    if (!a.bpart) S = 1;
+    if (S == 1) {
+        interp_kernel<T, Q, false><<<grid, kBlock, smem, st>>>(a);
+        return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+    }
+    if (cudaFuncSetAttribute(interp_kernel<T, Q, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return -1;
+    interp_kernel<T, Q, true><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a);
+    if (cudaPeekAtLastError() != cudaSuccess) return -1;
+    int64_t blocks = (a.nq + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    finalize_split_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(a, nblk);
+    return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 
 template <int Q, unsigned EMU, int STAGES, int BLOCK, bool SPLIT> static int interp_attrs(size_t smem)
@@ -388,7 +413,7 @@ static int launch_interp_f32x2(InterpArgs<float> a, cudaStream_t st, SplitBuf *s
     if (cudaPeekAtLastError() != cudaSuccess) return -1;
     int64_t blocks = (a.nq + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    finalize_split_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, nblk);
+    finalize_split_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(a, nblk);
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 
@@ -426,6 +451,12 @@ static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st, SplitB
     case 17: return launch_interp_f32x2<1, 0x0141, 4, 256>(a, st, sp);  // Q = 1, 256-thread CTAs
     case 18: return launch_interp_f32x2<1, 0x0141, 4, 512>(a, st, sp);  // Q = 1, 512-thread CTAs
     case 19: return launch_interp_f32x2<2, 0x0141, 4, 256>(a, st, sp);  // Q = 2, 256-thread CTAs
+    case 20: return launch_interp_f32x2<1, 0x1111>(a, st, sp);  // Q = 1, f = 4/8
+    case 21: return launch_interp_f32x2<1, 0x1115>(a, st, sp);  // Q = 1, f = 5/8
+    case 22: return launch_interp_f32x2<1, 0x0155>(a, st, sp);  // Q = 1, f = 4/8 (first half)
+    case 23: return launch_interp_f32x2<1, 0x2A2A>(a, st, sp);  // Q = 1, f = 3/8 split lanes
+    case 24: return launch_interp_f32x2<1, 0xAAAA>(a, st, sp);  // Q = 1, f = 1/2 split lanes
+    case 25: return launch_interp_f32x2<1, 0x4141>(a, st, sp);  // Q = 1, f = 4/8 (spread)
     default: return launch_interp_f32x2<1, 0x0141>(a, st, sp); // Q = 1, f = 3/8 packed (best measured, r01)
     }
 }
@@ -485,7 +516,7 @@ int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const vo
     InterpArgs<double> a{p, p + ndp, p + 2 * ndp, ndp, nd, (const double *)qx, (const double *)qy,
                          (const double *)alpha, (const double *)d1sq, nq, (double *)z, alpha_const, partial,
                          nullptr, nullptr};
-    return launch_interp_t<double, 2>(a, st);
+    return launch_interp_t<double, 2>(a, st, split);
 }
 
 }  // namespace aidw
