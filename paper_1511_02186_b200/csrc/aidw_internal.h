@@ -107,7 +107,7 @@ int launch_alpha(int dtype, const void *r_obs, int64_t nq, double r_exp, const d
                  int rb, double rmin, double rmax, const void *minmax, int mf, void *alpha,
                  cudaStream_t st);
 
-int launch_fused_fixed(const void *data, int64_t ndp, int64_t nd, const FilterData *filt, const void *qx,
+int launch_fused_fixed(const void *data, int64_t ndp, int64_t nd, FilterData *filt, const void *qx,
                        const void *qy, int64_t nq, int k, double r_exp, const double *lv, double rmin,
                        double rmax, int mf, void *z, void *r_obs, void *alpha, Scratch *sc, cudaStream_t st);
 

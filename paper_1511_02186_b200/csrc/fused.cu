@@ -28,6 +28,7 @@ struct FusedArgs {
     int mf;
     float *z, *r_obs, *alpha;  // r_obs / alpha nullable
     Scratch *sc;
+    const int *perm;  // nullable: launch slot i evaluates query perm[i] (spatial order, §4.7)
 };
 
 template <int K, int Q, int G, unsigned EMU>
@@ -41,6 +42,14 @@ __global__ void __launch_bounds__(kBlock) fused_fixed_kernel(const FusedArgs a)
                       reinterpret_cast<uint64_t *>(sm + STAGES * 5 * TILE) + STAGES};
     const int nt = (int)(a.ndp / TILE);
     const int ntot = 2 * nt;
+    // spatial order (§4.7): kNN tiles start under the CTA's queries and wrap around
+    int start = 0;
+    if (a.perm) {
+        const int64_t mid = min((int64_t)blockIdx.x * (kBlock * Q) + kBlock * Q / 2, a.nq - 1);
+        const int64_t qm = a.perm[mid];
+        start = a.f.cell_start[morton_cell(a.qx[qm], a.qy[qm], a.f.grid)] / TILE - 1;
+        start = start < 0 ? start + nt : (start >= nt ? nt - 1 : start);
+    }
     if (threadIdx.x == 0) ring.init();
     __syncthreads();
 
@@ -48,7 +57,8 @@ __global__ void __launch_bounds__(kBlock) fused_fixed_kernel(const FusedArgs a)
         constexpr uint32_t B = TILE * sizeof(float);
         float *d = sm + slot * 5 * TILE;
         if (gt < nt) {
-            const int64_t off = (int64_t)gt * TILE;
+            const int pt = gt + start < nt ? gt + start : gt + start - nt;
+            const int64_t off = (int64_t)pt * TILE;
             mbar_arrive_expect_tx(&ring.full[slot], 5u * B);
             bulk_g2s(d, a.f.cx + off, B, &ring.full[slot]);
             bulk_g2s(d + TILE, a.f.cy + off, B, &ring.full[slot]);
@@ -69,10 +79,11 @@ __global__ void __launch_bounds__(kBlock) fused_fixed_kernel(const FusedArgs a)
     const int64_t base = (int64_t)blockIdx.x * (kBlock * Q) + threadIdx.x;
     float qx[Q], qy[Q];
     bool valid[Q];
+    int64_t qid[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        const int64_t idx = base + q * kBlock;
-        valid[q] = idx < a.nq;
+        valid[q] = base + q * kBlock < a.nq;
+        const int64_t idx = qid[q] = (a.perm && valid[q]) ? (int64_t)a.perm[base + q * kBlock] : base + q * kBlock;
         qx[q] = valid[q] ? a.qx[idx] : 0.f;
         qy[q] = valid[q] ? a.qy[idx] : 0.f;
         if (valid[q] && !(isfinite(qx[q]) && isfinite(qy[q]))) atomicMin(&a.sc->err_idx, (long long)idx);
@@ -97,7 +108,7 @@ __global__ void __launch_bounds__(kBlock) fused_fixed_kernel(const FusedArgs a)
             float robs;
             robs_of<float, K>(st.buf[q], k0, a.k, robs, d1[q]);
             al[q] = (float)alpha_eq((double)robs, a.r_exp, a.rmin, a.rmax, a.mf, a.lv);
-            const int64_t idx = base + q * kBlock;
+            const int64_t idx = qid[q];
             if (valid[q]) {
                 if (a.r_obs) a.r_obs[idx] = robs;
                 if (a.alpha) a.alpha[idx] = al[q];
@@ -127,7 +138,7 @@ __global__ void __launch_bounds__(kBlock) fused_fixed_kernel(const FusedArgs a)
         if (!valid[q]) continue;
         double zq = st2.SWZ[q] / st2.SW[q];
         if (d1[q] == 0.f) zq = coincident_mean<float>(qx[q], qy[q], a.px, a.py, a.pz, a.nd);  // R19
-        a.z[base + q * kBlock] = (float)zq;
+        a.z[qid[q]] = (float)zq;
     }
 }
 
@@ -146,7 +157,16 @@ static int launch_fused_t(const FusedArgs &a, cudaStream_t st)
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-int launch_fused_fixed(const void *data, int64_t ndp, int64_t nd, const FilterData *filt, const void *qx,
+static int dispatch_fused(const FusedArgs &a, cudaStream_t st);
+
+// Batches at least this large are spatially ordered (AIDW_KNN_ORDER=0 disables).
+static bool order_fused(int64_t nq)
+{
+    const char *e = getenv("AIDW_KNN_ORDER");
+    return nq >= 32768 && !(e && e[0] == '0');
+}
+
+int launch_fused_fixed(const void *data, int64_t ndp, int64_t nd, FilterData *filt, const void *qx,
                        const void *qy, int64_t nq, int k, double r_exp, const double *lvp, double rmin,
                        double rmax, int mf, void *z, void *r_obs, void *alpha, Scratch *sc, cudaStream_t st)
 {
@@ -173,6 +193,26 @@ int launch_fused_fixed(const void *data, int64_t ndp, int64_t nd, const FilterDa
     a.r_obs = (float *)r_obs;
     a.alpha = (float *)alpha;
     a.sc = sc;
+    a.perm = nullptr;
+    int pre = 0;
+    if (filt->cell_start && order_fused(nq)) {  // spatial order (§4.7): Morton-sorted kNN copy
+        pre = launch_order_queries((const float *)qx, (const float *)qy, nq, filt, &filt->qorder, &a.perm, st);
+        if (pre < 0) return -1;
+        if (a.perm) {
+            a.f.cx = c + 3 * ndp;
+            a.f.cy = c + 4 * ndp;
+            a.f.pp = c + 5 * ndp;
+            a.f.px = c + 6 * ndp;
+            a.f.py = c + 7 * ndp;
+        }
+    }
+    const int n = dispatch_fused(a, st);
+    return n < 0 ? -1 : n + pre;
+}
+
+static int dispatch_fused(const FusedArgs &a, cudaStream_t st)
+{
+    const int k = a.k;
     if (k <= 1) return launch_fused_t<1>(a, st);
     if (k <= 2) return launch_fused_t<2>(a, st);
     if (k <= 4) return launch_fused_t<4>(a, st);

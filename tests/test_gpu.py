@@ -300,8 +300,9 @@ def test_split_bit_identical(P, monkeypatch, dtype, nd, nq, k):
 def test_knn_order_bit_identical(P, orc, monkeypatch, case):
     """Spatial order (Morton-sorted data copy, query permutation, per-CTA
     start tile) changes only the visiting order of the brute-force kNN: lists, r_obs,
-    d1sq, bounds and Z are bit-identical to the unordered launch, and exact vs the
-    oracle's float instantiation on sampled queries."""
+    d1sq, bounds and Z (stage kernels and the fused FIXED kernel) are bit-identical to
+    the unordered launches, and exact vs the oracle's float instantiation on sampled
+    queries."""
     if case == "C3":
         x, y, z = datagen.make_data("C3")
         qx, qy = datagen.make_queries("C3")
@@ -324,7 +325,8 @@ def test_knn_order_bit_identical(P, orc, monkeypatch, case):
             monkeypatch.setenv("AIDW_KNN_ORDER", sv)
         r, d1, mm, dd = eng.knn_robs(qx, qy, k, want_dists=True)
         zr = eng.run(qx, qy, k, LV, P.GLOBAL)
-        res[sv] = [t.cpu().numpy() for t in (r, d1, mm, dd, zr)]
+        zf, tf = eng.run_fixed(qx, qy, k, LV, 0.0, 2.0, trace=True)  # N1 fused kernel, same order
+        res[sv] = [t.cpu().numpy() for t in (r, d1, mm, dd, zr, zf, tf["r_obs"], tf["alpha"])]
     for n, (u, v) in enumerate(zip(res[None], res["0"])):
         assert np.array_equal(u, v), n
     idx = np.random.default_rng(5).choice(len(qx), 300, replace=False)
