@@ -457,7 +457,17 @@ static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st, SplitB
     case 23: return launch_interp_f32x2<1, 0x2A2A>(a, st, sp);  // Q = 1, f = 3/8 split lanes
     case 24: return launch_interp_f32x2<1, 0xAAAA>(a, st, sp);  // Q = 1, f = 1/2 split lanes
     case 25: return launch_interp_f32x2<1, 0x4141>(a, st, sp);  // Q = 1, f = 4/8 (spread)
-    default: return launch_interp_f32x2<1, 0x0141>(a, st, sp); // Q = 1, f = 3/8 packed (best measured, r01)
+    case 26: return launch_interp_f32x2<2, 0x1115>(a, st, sp);  // Q = 2, f = 5/8
+    case 27: return launch_interp_f32x2<2, 0x1111, 3>(a, st, sp);  // Q = 2, f = 4/8, 3 stages
+    case 28: return launch_interp_f32x2<2, 0x4141>(a, st, sp);  // Q = 2, f = 4/8 (spread)
+    case 29: return launch_interp_f32x2<2, 0x1111, 4, 256>(a, st, sp);  // Q = 2, f = 4/8, 256 threads
+    case 30: return launch_interp_f32x2<3, 0x1111>(a, st, sp);  // Q = 3, f = 4/8
+    case 31: return launch_interp_f32x2<2, 0x4141, 3>(a, st, sp);  // Q = 2, f = 4/8 spread, 3 stages
+    case 32: return launch_interp_f32x2<2, 0x1414>(a, st, sp);  // Q = 2, f = 4/8 spread (odd)
+    case 33: return launch_interp_f32x2<2, 0x4105>(a, st, sp);  // Q = 2, f = 4/8 (0, 1, 4, 7)
+    case 34: return launch_interp_f32x2<2, 0x0141>(a, st, sp);  // Q = 2, f = 3/8
+    case 35: return launch_interp_f32x2<1, 0x0141>(a, st, sp);  // Q = 1, f = 3/8 (default before v10)
+    default: return launch_interp_f32x2<2, 0x4141>(a, st, sp);  // Q = 2, f = 4/8 spread (best measured, r01 v10)
     }
 }
 

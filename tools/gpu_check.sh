@@ -17,3 +17,7 @@ for l in open("gpurun_out/configs.jsonl"):
 r=json.loads(open("gpurun_out/bench.json").read())
 print("bench", r["value"], r["ms_per_step"], r["phases_ms"], r["roofline"]["frac"], r["roofline"].get("path_frac"), r["clocks"])
 P
+timeout 600 python bench.py --mode fixed --no-cpu-baseline --no-e2e > gpurun_out/bench_fixed.json 2> gpurun_out/bench_fixed.err
+python -c "
+import json;r=json.load(open('gpurun_out/bench_fixed.json'))
+print('fixed', r['value'], r['ms_per_step'], r.get('phases_ms'))"

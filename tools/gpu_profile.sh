@@ -12,3 +12,7 @@ for K in interp_f32x2_kernel knn_filter_kernel; do
       -o gpurun_out/${TAG}_$K python bench.py --profile --warmup 0 > gpurun_out/${TAG}_$K.log 2>&1
 done
 ls -la gpurun_out | tail -8
+for K in interp_f32x2_kernel knn_filter_kernel; do
+  python tools/ncu_summary.py gpurun_out/${TAG}_$K.ncu-rep --json gpurun_out/${TAG}_$K.json > /dev/null 2>&1
+  ncu -i gpurun_out/${TAG}_$K.ncu-rep --page source --csv > gpurun_out/${TAG}_${K}_source.csv 2>/dev/null
+done
