@@ -50,15 +50,33 @@ KNN_FP32_PER_PAIR = 4     # canonical kNN distance (2 sub, mul, fma) -- SIMT FP3
 N_SM = 148
 
 
-def weight_clk_per_pair():
+def weight_clk_per_pair(fp32=WEIGHT_FP32_PER_PAIR, transc=TRANSC_PER_PAIR):
     """min over the SFU fraction of max(FMA-pipe time, SFU time), clocks per pair per SM."""
     best = None
     for i in range(0, 2001):
-        f = TRANSC_PER_PAIR * i / 2000.0  # transcendentals moved to the FMA pipe
-        t = max((WEIGHT_FP32_PER_PAIR + POLY_FMA_PER_TRANSC * f) / FMA_PER_CLK_SM,
-                (TRANSC_PER_PAIR - f) / MUFU_PER_CLK_SM)
+        f = transc * i / 2000.0  # transcendentals moved to the FMA pipe
+        t = max((fp32 + POLY_FMA_PER_TRANSC * f) / FMA_PER_CLK_SM, (transc - f) / MUFU_PER_CLK_SM)
         best = t if best is None else min(best, t)
     return best
+
+
+# Exact-exponent classes (DESIGN.md §4.3): a query whose alpha is exactly 1, 2 or 3 (and
+# whose d1^2 is in range) needs one transcendental per pair -- rsqrt, rcp or rsqrt^3 --
+# and s (4) + the two sums (2) [+ 2 FMUL for the cube] FP32 ops.
+CLASS_OPS = {"general": (WEIGHT_FP32_PER_PAIR, TRANSC_PER_PAIR), "a1": (6, 1), "a2": (6, 1), "a3": (8, 1)}
+
+
+def class_fractions(alpha, d1sq):
+    """Fraction of queries per weighting class (same rule as passes.cuh alpha_class)."""
+    ok = (d1sq >= 2.0 ** -78) & (d1sq <= 2.0 ** 66)
+    n = max(1, alpha.numel())
+    fr = {c: float(((alpha == v) & ok).sum()) / n for c, v in (("a1", 1.0), ("a2", 2.0), ("a3", 3.0))}
+    fr["general"] = 1.0 - sum(fr.values())
+    return fr
+
+
+def weight_clk_mix(fr):
+    return sum(f * weight_clk_per_pair(*CLASS_OPS[c]) for c, f in fr.items())
 
 
 def peaks():
@@ -372,7 +390,8 @@ def main():
     interp_ms = float(per[:, 3].mean())
     # dominant kernel: the weighting pass, bound by the SFU + FMA pipes together
     interp_rate = pairs / (interp_ms / 1e3)
-    w_clk = weight_clk_per_pair()
+    fr = class_fractions(al, d1) if args.mode != "fixed" else {"general": 1.0, "a1": 0.0, "a2": 0.0, "a3": 0.0}
+    w_clk = weight_clk_mix(fr)
     sfu_peak_pairs = N_SM * f_max / w_clk
     path_clk_per_pair = KNN_FP32_PER_PAIR / FMA_PER_CLK_SM + w_clk
     path_peak_pairs = N_SM * f_max / path_clk_per_pair
@@ -426,9 +445,12 @@ def main():
             "achieved": interp_rate / 1e9, "peak": sfu_peak_pairs / 1e9, "unit": "Gpair/s",
             "frac": interp_rate / sfu_peak_pairs, "traffic": traffic,
             "peak_basis": f"{N_SM} SM x {f_max / 1e6:.0f} MHz / {w_clk:.4f} clk per pair: 7 FP32 + 2 "
-                          f"transcendentals per pair split optimally between SFU ({MUFU_PER_CLK_SM}/clk) and "
-                          f"FMA pipe ({FMA_PER_CLK_SM}/clk, 8 ops per polynomial transcendental); measured pipe "
-                          f"rates profiles/r01_pipe_peaks.json; sm_max_mhz from MEASURED_PEAKS.json",
+                          f"transcendentals per pair (exact-exponent classes: 6-8 FP32 + 1) split optimally "
+                          f"between SFU ({MUFU_PER_CLK_SM}/clk) and FMA pipe ({FMA_PER_CLK_SM}/clk, 8 ops per "
+                          f"polynomial transcendental), weighted by the class mix; measured pipe rates "
+                          f"profiles/r01_pipe_peaks.json; sm_max_mhz from MEASURED_PEAKS.json",
+            "class_mix": {c: round(f, 5) for c, f in fr.items()},
+            "general_clk_per_pair": weight_clk_per_pair(),
             "sfu_only_peak": N_SM * MUFU_PER_CLK_SM / TRANSC_PER_PAIR * f_max / 1e9,
             "path_frac": (pairs / (ms / 1e3)) / path_peak_pairs,
             "path_peak_basis": "kNN 4 FP32/pair on the FMA pipe + the weighting bound above, per SM",

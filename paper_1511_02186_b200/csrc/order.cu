@@ -27,33 +27,60 @@ __global__ void cell_hist_kernel(const float *__restrict__ x, const float *__res
         atomicAdd(&counts[morton_cell(x[i], y[i], g)], 1u);
 }
 
-// Exclusive scan of kCells counts by one CTA of 1024 threads (64 cells per thread);
-// writes start[0..kCells] (start[kCells] = total) and a cursor copy for the scatter.
+// Exclusive scan of kCells counts by one CTA of 32 warps: warp w owns the contiguous
+// chunk [w*2048, (w+1)*2048) and reads it coalesced into registers (64 per lane, all
+// loads in flight at once); warp totals are scanned in shared memory.  Writes
+// start[0..kCells] (start[kCells] = total) and a cursor copy for the scatter.
 constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads) cell_scan_kernel(const unsigned *__restrict__ counts,
                                                                  int *__restrict__ start, int *__restrict__ cursor)
 {
-    constexpr int per = kCells / kScanThreads;
-    __shared__ unsigned part[kScanThreads];
-    const int t = threadIdx.x;
-    unsigned sum = 0;
-    for (int i = 0; i < per; ++i) sum += counts[t * per + i];
-    part[t] = sum;
+    constexpr int kWarps = kScanThreads / 32, chunk = kCells / kWarps, per = chunk / 32, batch = 16;
+    __shared__ unsigned wtot[kWarps];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned *src = counts + w * chunk + lane;
+    unsigned tot = 0;
+    for (int i0 = 0; i0 < per; i0 += batch) {  // pass 1: warp total (batches of 16 loads in flight)
+        unsigned v[batch];
+#pragma unroll
+        for (int i = 0; i < batch; ++i) v[i] = src[(i0 + i) * 32];
+#pragma unroll
+        for (int i = 0; i < batch; ++i) tot += v[i];
+    }
+    tot = __reduce_add_sync(0xffffffffu, tot);
+    if (lane == 0) wtot[w] = tot;
     __syncthreads();
-    for (int o = 1; o < kScanThreads; o <<= 1) {  // Hillis-Steele inclusive scan
-        const unsigned v = t >= o ? part[t - o] : 0u;
-        __syncthreads();
-        part[t] += v;
-        __syncthreads();
+    if (w == 0) {  // exclusive scan of the warp totals
+        const unsigned x = wtot[lane];
+        unsigned incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        wtot[lane] = incl - x;
+        if (lane == 31) start[kCells] = (int)incl;
     }
-    unsigned run = part[t] - sum;
-    for (int i = 0; i < per; ++i) {
-        const int c = t * per + i;
-        start[c] = (int)run;
-        if (cursor) cursor[c] = (int)run;
-        run += counts[c];
+    __syncthreads();
+    unsigned run = wtot[w];
+    for (int i0 = 0; i0 < per; i0 += batch) {  // pass 2: re-read (L2) and scan
+        unsigned v[batch];
+#pragma unroll
+        for (int i = 0; i < batch; ++i) v[i] = src[(i0 + i) * 32];
+#pragma unroll
+        for (int i = 0; i < batch; ++i) {
+            unsigned incl = v[i];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int c = w * chunk + (i0 + i) * 32 + lane;
+            start[c] = (int)(run + incl - v[i]);
+            if (cursor) cursor[c] = (int)(run + incl - v[i]);
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
     }
-    if (t == kScanThreads - 1) start[kCells] = (int)run;
 }
 
 // Data: the centred filter values in the caller's order (for unordered launches) and,
