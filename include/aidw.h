@@ -27,6 +27,15 @@
  *  - No exceptions cross the ABI.  A handle is not thread-safe: use one handle
  *    per (device, stream) at a time.
  *  - nq == 0 is a successful no-op.  k must be in [1, 32], nd >= k.
+ *  - Launch shape never changes a result: the kNN outputs are exact, and Z is
+ *    bit-identical for any split of the data range, query order or GPU count
+ *    (DESIGN.md §4.6-4.7, §5).  The handle owns growable device scratch for the
+ *    small-nq data split and the spatial query order (allocated on first use).
+ *  - Tuning/testing environment variables (read per call; defaults are the
+ *    measured best): AIDW_SPLIT=0|n (data split off / forced factor),
+ *    AIDW_KNN_ORDER=0 (no spatial query order), AIDW_ALPHA_CLASSES=0 (no
+ *    exact-exponent weighting classes), AIDW_KNN_FILTER=0 (canonical fp32 kNN,
+ *    read at aidw_create), AIDW_KNN_VARIANT / AIDW_INTERP_VARIANT (tuning sweeps).
  */
 #ifndef AIDW_H
 #define AIDW_H

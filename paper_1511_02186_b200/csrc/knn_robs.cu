@@ -257,8 +257,8 @@ __global__ void __launch_bounds__(kBlock) knn_robs_kernel(const KnnArgs<T> a)
 
 // ---------------------------------------------------------------------------------
 // Filtered fp32 kernel (passes.cuh knn_f32_tile): smem tiles of (cx, cy, pp, x, y).
-template <int K, int Q, int G, bool SPLIT>
-__global__ void __launch_bounds__(kBlock) knn_filter_kernel(const KnnArgs<float> a, const FilterArgs f)
+template <int K, int Q, int G, bool SPLIT, int MINB = 1>
+__global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<float> a, const FilterArgs f)
 {
     constexpr int TILE = kTileKF, STAGES = kStagesKF;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -348,9 +348,9 @@ template <typename T> static int knn_finish(const KnnArgs<T> &a, int S, cudaStre
 }
 
 // ---------------------------------------------------------------------------------
-template <int K, int Q, int G, bool SPLIT> static int set_filter_attrs(size_t smem)
+template <int K, int Q, int G, bool SPLIT, int MINB> static int set_filter_attrs(size_t smem)
 {
-    auto kern = knn_filter_kernel<K, Q, G, SPLIT>;
+    auto kern = knn_filter_kernel<K, Q, G, SPLIT, MINB>;
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
                    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) == cudaSuccess
                ? 0
@@ -366,16 +366,16 @@ static bool order_queries(int64_t nq)
     return nq >= kOrderMinQ && !(e && e[0] == '0');
 }
 
-template <int K, int Q, int G = 8>
+template <int K, int Q, int G = 8, int MINB = 1>
 static int launch_knn_filter_t(KnnArgs<float> a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp,
                                FilterData *fd)
 {
     const size_t smem = (size_t)5 * kStagesKF * kTileKF * sizeof(float) + 2 * kStagesKF * sizeof(uint64_t);
-    if (set_filter_attrs<K, Q, G, false>(smem) < 0) return -1;
+    if (set_filter_attrs<K, Q, G, false, MINB>(smem) < 0) return -1;
     const int64_t per_cta = (int64_t)kBlock * Q;
     const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
     const int S =
-        knn_split_factor((const void *)knn_filter_kernel<K, Q, G, false>, smem, grid, (int)(a.ndp / kTileKF), a, sp);
+        knn_split_factor((const void *)knn_filter_kernel<K, Q, G, false, MINB>, smem, grid, (int)(a.ndp / kTileKF), a, sp);
     int pre = 0;
     if (S == 1) {
         FilterArgs fo = f;
@@ -391,10 +391,10 @@ static int launch_knn_filter_t(KnnArgs<float> a, const FilterArgs &f, cudaStream
                 fo.py = c + 7 * a.ndp;
             }
         }
-        knn_filter_kernel<K, Q, G, false><<<grid, kBlock, smem, st>>>(a, fo);
+        knn_filter_kernel<K, Q, G, false, MINB><<<grid, kBlock, smem, st>>>(a, fo);
     } else {
-        if (set_filter_attrs<K, Q, G, true>(smem) < 0) return -1;
-        knn_filter_kernel<K, Q, G, true><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, f);
+        if (set_filter_attrs<K, Q, G, true, MINB>(smem) < 0) return -1;
+        knn_filter_kernel<K, Q, G, true, MINB><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, f);
     }
     const int n = knn_finish(a, S, st);
     return n < 0 ? -1 : n + pre;
@@ -424,6 +424,10 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
         case 7: return launch_knn_filter_t<10, 2, 32>(a, f, st, sp, fd);
         case 8: return launch_knn_filter_t<10, 4, 32>(a, f, st, sp, fd);
         case 9: return launch_knn_filter_t<10, 3, 32>(a, f, st, sp, fd);
+        case 10: return launch_knn_filter_t<10, 4, 32, 5>(a, f, st, sp, fd);
+        case 11: return launch_knn_filter_t<10, 4, 16, 5>(a, f, st, sp, fd);
+        case 12: return launch_knn_filter_t<10, 3, 32, 6>(a, f, st, sp, fd);
+        case 13: return launch_knn_filter_t<10, 2, 32, 8>(a, f, st, sp, fd);
         default: break;
         }
     }
