@@ -31,11 +31,12 @@
  *    bit-identical for any split of the data range, query order or GPU count
  *    (DESIGN.md §4.6-4.7, §5).  The handle owns growable device scratch for the
  *    small-nq data split and the spatial query order (allocated on first use).
- *  - Tuning/testing environment variables (read per call; defaults are the
- *    measured best): AIDW_SPLIT=0|n (data split off / forced factor),
- *    AIDW_KNN_ORDER=0 (no spatial query order), AIDW_ALPHA_CLASSES=0 (no
- *    exact-exponent weighting classes), AIDW_KNN_FILTER=0 (canonical fp32 kNN,
- *    read at aidw_create), AIDW_KNN_VARIANT / AIDW_INTERP_VARIANT (tuning sweeps).
+ *  - Tuning/testing environment variables (defaults are the measured best):
+ *    AIDW_SPLIT=0|n (data split off / forced factor) and AIDW_KNN_ORDER=0 (no
+ *    spatial query order) are read per call; AIDW_ALPHA_CLASSES=0 (no
+ *    exact-exponent weighting classes) and AIDW_KNN_VARIANT / AIDW_INTERP_VARIANT
+ *    (tuning sweeps) once per process; AIDW_KNN_FILTER=0 (canonical fp32 kNN) at
+ *    aidw_create.
  */
 #ifndef AIDW_H
 #define AIDW_H
