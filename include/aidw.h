@@ -28,7 +28,8 @@
  *    per (device, stream) at a time.
  *  - nq == 0 is a successful no-op.  k must be in [1, 32], nd >= k.
  *  - Launch shape never changes a result: the kNN outputs are exact, and Z is
- *    bit-identical for any split of the data range, query order or GPU count
+ *    bit-identical for any in-GPU split of the data range, query order or GPU count
+ *    of the query-sharded path
  *    (DESIGN.md §4.6-4.7, §5).  The handle owns growable device scratch for the
  *    small-nq data split and the spatial query order (allocated on first use).
  *  - Tuning/testing environment variables (defaults are the measured best):
