@@ -347,3 +347,57 @@ class AIDW:
 
     def check(self, stream=None):
         aidw_check(self.h, stream)
+
+    # ---- CUDA graph of the whole path for a fixed batch shape (serving loops)
+    def capture(self, nq, k=10, levels=LEVELS_DEFAULT, rbounds=GLOBAL, r_min=0.0, r_max=2.0,
+                muform=NORMALIZED, group=None):
+        """Capture S1..S5 for batches of ``nq`` queries into one CUDA graph.
+
+        Returns an :class:`AidwGraph` whose static ``qx`` / ``qy`` device buffers the
+        caller fills before :meth:`AidwGraph.replay`; ``z`` (and ``r_obs``, ``alpha``)
+        hold the results.  One eager warm-up sizes the handle's scratch first (no
+        allocation may happen inside a capture).  Replays launch the same kernels
+        with the same launch shapes as an eager :meth:`run`, so results are
+        bit-identical to it."""
+        return AidwGraph(self, nq, k, levels, rbounds, r_min, r_max, muform, group)
+
+
+class AidwGraph:
+    """A captured AIDW step (see :meth:`AIDW.capture`)."""
+
+    def __init__(self, eng, nq, k, levels, rbounds, r_min, r_max, muform, group):
+        from .partition import allreduce_bounds
+        self.eng, self.nq = eng, int(nq)
+        self.qx, self.qy = eng._empty(self.nq), eng._empty(self.nq)
+        self.qx.zero_()
+        self.qy.zero_()
+        self.r_obs, self.d1sq, self.alpha, self.z = (eng._empty(self.nq) for _ in range(4))
+        self.minmax = eng._empty(2)
+        lv = tuple(float(v) for v in levels)
+
+        def step():
+            st = torch.cuda.current_stream(eng.device)
+            aidw_knn_robs(eng.h, self.qx, self.qy, k, self.r_obs, self.d1sq, self.minmax, None, st)
+            if rbounds == GLOBAL and group is not None:
+                allreduce_bounds(self.minmax, group)
+            aidw_alpha(eng.h, self.r_obs, lv, rbounds, r_min, r_max, self.minmax, muform, self.alpha, st)
+            aidw_interpolate(eng.h, self.qx, self.qy, self.alpha, self.d1sq, self.z, st)
+
+        side = torch.cuda.Stream(eng.device)
+        side.wait_stream(torch.cuda.current_stream(eng.device))
+        with torch.cuda.device(eng.device), torch.cuda.stream(side):
+            step()  # warm-up: sizes the split / order scratch outside the capture
+        torch.cuda.current_stream(eng.device).wait_stream(side)
+        torch.cuda.synchronize(eng.device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.device(eng.device), torch.cuda.graph(self.graph):
+            step()
+
+    def replay(self, qx=None, qy=None):
+        """Copy new queries into the static buffers (optional) and replay the graph."""
+        if qx is not None:
+            self.qx.copy_(torch.as_tensor(qx, dtype=self.qx.dtype).reshape(-1), non_blocking=True)
+        if qy is not None:
+            self.qy.copy_(torch.as_tensor(qy, dtype=self.qy.dtype).reshape(-1), non_blocking=True)
+        self.graph.replay()
+        return self.z

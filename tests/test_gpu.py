@@ -334,6 +334,23 @@ def test_knn_order_bit_identical(P, orc, monkeypatch, case):
     assert np.array_equal(res[None][0][idx], ro)
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("nq", [777, 40000])
+def test_graph_replay_bit_identical(P, dtype, nq):
+    """The whole path captured as one CUDA graph (AIDW.capture) replays with new queries
+    and gives bit-identical results to eager runs (same kernels, same launch shapes)."""
+    x, y, z, qx, qy = datagen.random_cloud(900 + nq, 50000, nq)
+    eng = P.AIDW(x, y, z, dtype=dtype)
+    g = eng.capture(nq, 10, LV, P.GLOBAL)
+    for seed in (1, 2):
+        _, _, _, qx2, qy2 = datagen.random_cloud(seed, 10, nq)
+        zg = g.replay(qx2, qy2).clone()
+        torch.cuda.synchronize()
+        ze, te = eng.run(qx2, qy2, 10, LV, P.GLOBAL, trace=True)
+        assert torch.equal(zg, ze)
+        assert torch.equal(g.r_obs, te["r_obs"]) and torch.equal(g.alpha, te["alpha"])
+
+
 def test_errors(P):
     x, y, z, qx, qy = datagen.random_cloud(1, 100, 10)
     with pytest.raises(P.AidwError, match="DEGENERATE"):
