@@ -107,7 +107,7 @@ aidw_status ensure_work(aidw_t h, size_t bytes)
 // fp64).  AIDW_ALPHA_CLASSES=0 disables the exact-exponent paths.
 int *perm_for(aidw_t h, int64_t nq)
 {
-    if (h->dt != AIDW_F32) return nullptr;
+    if (h->dt != AIDW_F32 || nq > INT_MAX) return nullptr;  // the permutation is int32
     static int enabled = -1;
     if (enabled < 0) {
         const char *e = getenv("AIDW_ALPHA_CLASSES");

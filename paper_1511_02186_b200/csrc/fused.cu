@@ -13,6 +13,8 @@
 // mode (same tile functions, same operation order).
 #include "passes.cuh"
 
+#include <climits>
+
 namespace aidw {
 
 struct FusedArgs {
@@ -163,7 +165,7 @@ static int dispatch_fused(const FusedArgs &a, cudaStream_t st);
 static bool order_fused(int64_t nq)
 {
     const char *e = getenv("AIDW_KNN_ORDER");
-    return nq >= 32768 && !(e && e[0] == '0');
+    return nq >= 32768 && nq <= INT_MAX && !(e && e[0] == '0');  // perm is int32
 }
 
 int launch_fused_fixed(const void *data, int64_t ndp, int64_t nd, FilterData *filt, const void *qx,

@@ -363,7 +363,7 @@ static bool order_queries(int64_t nq)
 {
     constexpr int64_t kOrderMinQ = 32768;
     const char *e = getenv("AIDW_KNN_ORDER");
-    return nq >= kOrderMinQ && !(e && e[0] == '0');
+    return nq >= kOrderMinQ && nq <= INT_MAX && !(e && e[0] == '0');  // perm is int32
 }
 
 template <int K, int Q, int G = 8, int MINB = 1>
@@ -428,6 +428,8 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
         case 11: return launch_knn_filter_t<10, 4, 16, 5>(a, f, st, sp, fd);
         case 12: return launch_knn_filter_t<10, 3, 32, 6>(a, f, st, sp, fd);
         case 13: return launch_knn_filter_t<10, 2, 32, 8>(a, f, st, sp, fd);
+        case 14: return launch_knn_filter_t<10, 1, 16>(a, f, st, sp, fd);
+        case 15: return launch_knn_filter_t<10, 1, 32>(a, f, st, sp, fd);
         default: break;
         }
     }
