@@ -450,6 +450,7 @@ def main():
                           f"polynomial transcendental), weighted by the class mix; measured pipe rates "
                           f"profiles/r01_pipe_peaks.json; sm_max_mhz from MEASURED_PEAKS.json",
             "class_mix": {c: round(f, 5) for c, f in fr.items()},
+            "hbm_gb_per_s": (traffic / (interp_ms / 1e3) / 1e9) if traffic else None,
             "general_clk_per_pair": weight_clk_per_pair(),
             "sfu_only_peak": N_SM * MUFU_PER_CLK_SM / TRANSC_PER_PAIR * f_max / 1e9,
             "path_frac": (pairs / (ms / 1e3)) / path_peak_pairs,
