@@ -257,7 +257,9 @@ __global__ void __launch_bounds__(kBlock) knn_robs_kernel(const KnnArgs<T> a)
 
 // ---------------------------------------------------------------------------------
 // Filtered fp32 kernel (passes.cuh knn_f32_tile): smem tiles of (cx, cy, pp, x, y).
-template <int K, int Q, int G, bool SPLIT, int MINB = 1>
+// MINB = 0: no occupancy hint (an explicit minBlocks of 1 lets ptxas use up to 255
+// registers and was measured slower: 113 vs 108 ms at C4).
+template <int K, int Q, int G, bool SPLIT, int MINB = 0>
 __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<float> a, const FilterArgs f)
 {
     constexpr int TILE = kTileKF, STAGES = kStagesKF;
@@ -366,7 +368,7 @@ static bool order_queries(int64_t nq)
     return nq >= kOrderMinQ && nq <= INT_MAX && !(e && e[0] == '0');  // perm is int32
 }
 
-template <int K, int Q, int G = 8, int MINB = 1>
+template <int K, int Q, int G = 8, int MINB = 0>
 static int launch_knn_filter_t(KnnArgs<float> a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp,
                                FilterData *fd)
 {
