@@ -32,6 +32,13 @@ for dt in (torch.float32, torch.float64):
     for v in (0, 1):
         P.aidw_paper_baseline(v, t, len(x), torch.as_tensor(qx, dtype=dt, device="cuda"),
                               torch.as_tensor(qy, dtype=dt, device="cuda"), 10, LV, eng.area, 0, 2, zo)
+    # large batch: spatial query order + Q = 4 kNN (fp32), unsplit launches
+    _, _, _, bx, by = datagen.random_cloud(6, 10, 40000)
+    eng.run(bx, by, 10, LV, P.GLOBAL)
+    eng.run_fixed(bx, by, 10)
+    os.environ["AIDW_SPLIT"] = "0"
+    eng.run(qx, qy, 10, LV, P.GLOBAL)
+    del os.environ["AIDW_SPLIT"]
     torch.cuda.synchronize()
     eng.check()
 print("sanitize run ok")
