@@ -35,13 +35,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--configs", default="C1,C2,C3,C4,C5")
+    ap.add_argument("--dtypes", default=None, help="override the configs' precisions, e.g. f64")
     args = ap.parse_args()
     res = []
     for name in args.configs.split(","):
         cfg = datagen.CONFIGS[name]
         x, y, z = datagen.make_data(name)
         qx, qy = datagen.make_queries(name)
-        for dt_name in cfg["dtypes"]:
+        for dt_name in (args.dtypes.split(",") if args.dtypes else cfg["dtypes"]):
             dt = torch.float32 if dt_name == "f32" else torch.float64
             eng = P.AIDW(x, y, z, dtype=dt)
             dev = torch.device("cuda")

@@ -41,6 +41,19 @@ __global__ void bench(float *out, Clk *clk, float seed)
                     float2 b = *reinterpret_cast<float2 *>(&r);
                     v[i] = b.x; v[i + 1] = b.y;
                 }
+            } else if (MODE == 7) {  // FFMA2 with a broadcast scalar multiplier (kNN filter form)
+                if (i % 2 == 0) {
+                    float2 a = make_float2(v[i], v[i + 1]);
+                    float2 b = __ffma2_rn(make_float2(seed, seed), a, make_float2(1e-7f, 2e-7f));
+                    v[i] = b.x; v[i + 1] = b.y;
+                }
+            } else if (MODE == 8) {  // the filter's dependent pair: t = B*cy + (A*cx + pp)
+                if (i % 4 == 0) {
+                    float2 cx = make_float2(v[i], v[i + 1]), cy = make_float2(v[i + 2], v[i + 3]);
+                    float2 t = __ffma2_rn(make_float2(seed, seed), cx, make_float2(1e-7f, 2e-7f));
+                    t = __ffma2_rn(make_float2(seed * 0.5f, seed * 0.5f), cy, t);
+                    v[i] = t.x; v[i + 1] = t.y; v[i + 2] = t.y; v[i + 3] = t.x;
+                }
             } else {                                                        // MUFU + FFMA mix 1:7
                 if (i == 0) v[i] = ex2(v[i]);
                 else v[i] = fmaf(v[i], 1.0000001f, 1e-7f);
@@ -83,6 +96,10 @@ int main()
     double m5, m6;
     double rs = run<5>(sms, out, clk, &m5), rc = run<6>(sms, out, clk, &m6);
     printf("{\"mufu_rsq_per_clk_sm\": %.2f, \"mufu_rcp_per_clk_sm\": %.2f}\n", rs, rc);
+    double m7, m8;
+    double b7 = run<7>(sms, out, clk, &m7), b8 = run<8>(sms, out, clk, &m8);
+    // mode 7: values updated = 2 FMAs per FFMA2; mode 8: 2 FFMA2 (4 FMAs) per 4 values
+    printf("{\"ffma2_bcast_fma_per_clk_sm\": %.2f, \"ffma2_filter_pair_fma_per_clk_sm\": %.2f}\n", b7, b8);
     // modes 3/4 count values updated: mode 3 = FMAs (2 per FFMA2 instruction), mode 4 = 1 ex2 + 7 FFMA
     printf("{\"sms\": %d, \"mufu_ex2_per_clk_sm\": %.2f, \"mufu_lg2_per_clk_sm\": %.2f, \"ffma_per_clk_sm\": %.2f, "
            "\"ffma2_fma_per_clk_sm\": %.2f, \"ffma2_instr_per_clk_sm\": %.2f, \"mix_1ex2_7ffma_ops_per_clk_sm\": %.2f, "
