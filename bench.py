@@ -223,6 +223,9 @@ def main():
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no baselines, no flush)")
     ap.add_argument("--nq", type=int, default=NQ_PER_GPU, help="queries per GPU (default C4)")
     ap.add_argument("--ref-queries-per-step", type=int, default=0)
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="GLOBAL bounds: NCCL allreduce(MAX) (default) or the device-side push over "
+                         "peer memory (aidw_exchange_*, no collective per step)")
     ap.add_argument("--mode", default="global", choices=["global", "fixed", "fixed3"],
                     help="global: 3 kernels + allreduce (north star, default); fixed: R bounds (0, 2), "
                          "one fused kernel per step (N1); fixed3: R bounds (0, 2) on the stage kernels")
@@ -263,6 +266,10 @@ def main():
     st = torch.cuda.current_stream(dev)
     flush = None if args.profile else torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
 
+    exchange = args.exchange == "p2p" and args.mode == "global"
+    if exchange:  # device-side bounds exchange over peer memory
+        from paper_1511_02186_b200.partition import connect_exchange
+        connect_exchange(eng, group)
     r_obs = torch.empty(nq, dtype=torch.float32, device=dev)
     d1 = torch.empty_like(r_obs)
     al = torch.empty_like(r_obs)
@@ -282,13 +289,13 @@ def main():
         if ev: ev[0].record(st)
         P.aidw_knn_robs(eng.h, qx, qy, K_NN, r_obs, d1, mm, None, st)
         if ev: ev[1].record(st)
-        if group is not None and args.mode == "global":
+        if group is not None and args.mode == "global" and not exchange:
             allreduce_bounds(mm, group)
         if ev: ev[2].record(st)
         if args.mode == "fixed3":
             P.aidw_alpha(eng.h, r_obs, lv, P.FIXED, 0.0, 2.0, mm, P.NORMALIZED, al, st)
-        else:
-            P.aidw_alpha(eng.h, r_obs, lv, P.GLOBAL, 0.0, 0.0, mm, P.NORMALIZED, al, st)
+        else:  # with --exchange p2p the alpha kernel reads the peers' pushed bounds (mm = NULL)
+            P.aidw_alpha(eng.h, r_obs, lv, P.GLOBAL, 0.0, 0.0, None if exchange else mm, P.NORMALIZED, al, st)
         if ev: ev[3].record(st)
         P.aidw_interpolate(eng.h, qx, qy, al, d1, zo, st)
         if ev: ev[4].record(st)
@@ -354,7 +361,7 @@ def main():
                 dy = hy.to(dev, non_blocking=True)
                 zz = eng.run_fixed(dx, dy, K_NN, lv, 0.0, 2.0)
                 hz.copy_(zz, non_blocking=True)
-            elif group is None:
+            elif group is None and not exchange:
                 eng.run_host(hx, hy, K_NN, lv, P.GLOBAL, out=hz)  # C ABI aidw_run_host
             else:
                 dx = hx.to(dev, non_blocking=True)
@@ -373,7 +380,8 @@ def main():
                "h2d_bytes_per_step": 2 * 4 * nq * world, "d2h_bytes_per_step": 4 * nq * world,
                "api": ("aidw_run_fixed + torch H2D/D2H (pinned)" if args.mode == "fixed" else
                        "AIDW.run(FIXED) + torch H2D/D2H (pinned)" if args.mode == "fixed3" else
-                       "aidw_run_host (C ABI, pinned host buffers)" if group is None else
+                       "aidw_run_host (C ABI, pinned host buffers)" if group is None and not exchange else
+                       "AIDW.run + torch H2D/D2H (pinned), device-side bounds exchange" if exchange else
                        "AIDW.run + torch H2D/D2H (pinned), allreduce")}
 
     if rank != 0:
@@ -436,7 +444,9 @@ def main():
                                "fixed3": "fixed (0, 2), stage kernels"}[args.mode],
                    "mu": "normalized",
                    "l2": "flushed between steps (256 MiB write outside the timed events)",
-                   "parallelism": f"query-sharded x{world}, data replicated"},
+                   "parallelism": f"query-sharded x{world}, data replicated",
+                   "bounds_exchange": ("device push over peer memory (aidw_exchange_*)" if exchange else
+                                       "NCCL allreduce(MAX)" if world > 1 else "local")},
         "pair_evals_per_s": 2 * pairs * world / (ms / 1e3),
         "aidw_pairs_per_s": pairs * world / (ms / 1e3),
         "phases_ms": phases,

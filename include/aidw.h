@@ -255,6 +255,27 @@ AIDW_API aidw_status aidw_finalize(aidw_t h, const double *partials, int P, int6
                                    void *stream);
 
 /*
+ * Device-side GLOBAL-bounds exchange (SURVEY.md §8(f) N4 "device-initiated fused min/max
+ * push").  Replaces the host-issued allreduce(MAX) of {-min, max} r_obs
+ * between aidw_knn_robs and aidw_alpha (the north star's global R
+ * bounds) by peer-memory stores: once connected, the LAST CTA of each kNN launch writes
+ * its {-min, max} into every rank's exchange buffer over NVLink (CUDA IPC mappings,
+ * system-scope release), and aidw_alpha(GLOBAL, robs_minmax = NULL) waits on the
+ * device for all ranks of the same step (acquire loads), then takes the MAX.  Bounds
+ * are bit-identical to the allreduce (MAX is exact).  Every rank must call aidw_knn_robs
+ * (with robs_minmax != NULL; nq == 0 pushes the MAX identity) and aidw_alpha in step;
+ * a wait gives up after ~2 s and aidw_check then reports it.  One process per GPU;
+ * processes sharing a GPU also work (tests).  Not for aidw_run_host.
+ *   aidw_exchange_setup  : allocate this rank's buffer; ipc_handle_out receives 64 bytes
+ *                          (a cudaIpcMemHandle_t) to all-gather across ranks
+ *   aidw_exchange_connect: ipc_handles = world x 64 bytes in rank order; maps the peers
+ *   aidw_exchange_close  : unmap and free (also done by aidw_destroy)
+ */
+AIDW_API aidw_status aidw_exchange_setup(aidw_t h, int rank, int world, void *ipc_handle_out);
+AIDW_API aidw_status aidw_exchange_connect(aidw_t h, const void *ipc_handles);
+AIDW_API aidw_status aidw_exchange_close(aidw_t h);
+
+/*
  * aidw_run_host -- the whole single-GPU path from HOST buffers: H2D of the
  * queries, knn_robs, (GLOBAL: local bounds = the job's bounds), alpha,
  * interpolate, D2H of Z; synchronises `stream` and reports deferred errors.

@@ -45,7 +45,8 @@ EXPORTS = (
     "aidw_area", "aidw_r_exp", "aidw_dtype_of", "aidw_knn_robs", "aidw_alpha", "aidw_interpolate",
     "aidw_run_host", "aidw_check", "aidw_launch_count", "aidw_destroy", "aidw_run_fixed", "aidw_idw",
     "aidw_paper_baseline", "aidw_set_extent", "aidw_bbox", "aidw_knn_partial", "aidw_knn_merge",
-    "aidw_interpolate_partial", "aidw_finalize",
+    "aidw_interpolate_partial", "aidw_finalize", "aidw_exchange_setup", "aidw_exchange_connect",
+    "aidw_exchange_close",
 )
 
 
@@ -91,6 +92,9 @@ def lib():
             "aidw_knn_merge": ([P, P, I, I64, I, P, P, P, P], I),
             "aidw_interpolate_partial": ([P, P, P, I64, P, P, P, P], I),
             "aidw_finalize": ([P, P, I, I64, P, P], I),
+            "aidw_exchange_setup": ([P, I, I, P], I),
+            "aidw_exchange_connect": ([P, P], I),
+            "aidw_exchange_close": ([P], I),
             "aidw_destroy": ([P], I),
         }
         for name, (args, res) in sig.items():
@@ -207,6 +211,7 @@ class AIDW:
             self.h = aidw_create(data, self.nd, self.dt, SOA, area, self.device.index)
         self.r_exp = lib().aidw_r_exp(self.h)
         self.area = lib().aidw_area(self.h)
+        self.exchanged = False
 
     def close(self):
         if getattr(self, "h", None):
@@ -264,6 +269,14 @@ class AIDW:
         nvtx.range_push("aidw.knn_robs")  # NVTX ranges for Nsight timelines (SURVEY §5 tracing)
         r_obs, d1sq, mm = self.knn_robs(qx, qy, k, stream=stream)
         nvtx.range_pop()
+        if rbounds == GLOBAL and self.exchanged:  # bounds pushed/read on the device (§5)
+            nvtx.range_push("aidw.alpha")
+            a = self.alpha(r_obs, levels, rbounds, r_min, r_max, None, muform, stream)
+            nvtx.range_pop()
+            z = self.interpolate(qx, qy, a, d1sq, stream)
+            if trace:
+                return z, dict(r_obs=r_obs, d1sq=d1sq, minmax=mm, alpha=a)
+            return z
         if rbounds == GLOBAL and group is not None:
             nvtx.range_push("aidw.allreduce_bounds")
             allreduce_bounds(mm, group)
@@ -334,6 +347,23 @@ class AIDW:
         _err(self.h, lib().aidw_finalize(self.h, _ptr(partials), int(P), int(nq), _ptr(z), _stream(stream)))
         return z
 
+    # ---- device-side GLOBAL-bounds exchange (N4 push; aidw_exchange_*)
+    def exchange_setup(self, rank, world) -> bytes:
+        """Allocate this rank's exchange buffer; returns its 64-byte IPC handle."""
+        buf = ctypes.create_string_buffer(64)
+        _err(self.h, lib().aidw_exchange_setup(self.h, int(rank), int(world), buf))
+        return buf.raw
+
+    def exchange_connect(self, handles):
+        """Map every rank's buffer (``handles``: the all-gathered 64-byte handles)."""
+        blob = b"".join(handles)
+        _err(self.h, lib().aidw_exchange_connect(self.h, ctypes.c_char_p(blob)))
+        self.exchanged = True
+
+    def exchange_close(self):
+        _err(self.h, lib().aidw_exchange_close(self.h))
+        self.exchanged = False
+
     def run_host(self, qx_host, qy_host, k=10, levels=LEVELS_DEFAULT, rbounds=GLOBAL, r_min=0.0, r_max=2.0,
                  muform=NORMALIZED, out=None, stream=None):
         """Single-GPU path from HOST buffers through the C ABI (aidw_run_host)."""
@@ -378,9 +408,11 @@ class AidwGraph:
         def step():
             st = torch.cuda.current_stream(eng.device)
             aidw_knn_robs(eng.h, self.qx, self.qy, k, self.r_obs, self.d1sq, self.minmax, None, st)
-            if rbounds == GLOBAL and group is not None:
+            exch = rbounds == GLOBAL and eng.exchanged  # bounds from the device-side exchange
+            if rbounds == GLOBAL and group is not None and not exch:
                 allreduce_bounds(self.minmax, group)
-            aidw_alpha(eng.h, self.r_obs, lv, rbounds, r_min, r_max, self.minmax, muform, self.alpha, st)
+            aidw_alpha(eng.h, self.r_obs, lv, rbounds, r_min, r_max, None if exch else self.minmax, muform,
+                       self.alpha, st)
             aidw_interpolate(eng.h, self.qx, self.qy, self.alpha, self.d1sq, self.z, st)
 
         side = torch.cuda.Stream(eng.device)

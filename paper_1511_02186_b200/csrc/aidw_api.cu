@@ -24,6 +24,12 @@ struct aidw_ctx {
     int *perm = nullptr;             // weighting-pass class permutation (fp32)
     int64_t perm_cap = 0;
     aidw::SplitBuf split;            // small-nq data split scratch
+    // GLOBAL-bounds exchange over peer memory
+    aidw::ExBuf *ex_own = nullptr;   // this rank's buffer (peers write into it)
+    aidw::ExBuf **ex_peers_dev = nullptr;
+    aidw::ExBuf *ex_mapped[aidw::kExMaxRanks] = {};  // IPC-opened peer buffers
+    int ex_rank = -1, ex_world = 0;
+    bool ex_connected = false;
     int64_t launches = 0;
     double bbox[4] = {0, 0, 0, 0};
     char err[512] = {0};
@@ -331,8 +337,14 @@ aidw_status aidw_knn_robs(aidw_t h, const void *qx, const void *qy, int64_t nq, 
     if (nq > (int64_t)1 << 40) return fail(h, AIDW_E_UNSUPPORTED, "nq too large");
     CK(h, cudaSetDevice(h->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (h->ex_connected && !robs_minmax)
+        return fail(h, AIDW_E_INVALID_ARG, "the bounds exchange needs robs_minmax (peers wait for it)");
     if (nq == 0) {
-        if (robs_minmax) return launched(h, aidw::launch_minmax_identity((int)h->dt, robs_minmax, st), "minmax");
+        if (robs_minmax) {
+            aidw_status s = launched(h, aidw::launch_minmax_identity((int)h->dt, robs_minmax, st), "minmax");
+            if (s != AIDW_OK || !h->ex_connected) return s;
+            return launched(h, aidw::launch_exchange_push_identity(h->sc, st), "exchange push");
+        }
         return AIDW_OK;
     }
     return launched(h,
@@ -355,16 +367,103 @@ aidw_status aidw_alpha(aidw_t h, const void *r_obs, int64_t nq, const double *al
         if (!(std::isfinite(r_min) && std::isfinite(r_max)))
             return fail(h, AIDW_E_INVALID_BOUNDS, "r_min/r_max must be finite");
         if (!(r_min < r_max)) return fail(h, AIDW_E_INVALID_BOUNDS, "r_min = %g >= r_max = %g", r_min, r_max);
-    } else if (nq > 0 && !robs_minmax) {
-        return fail(h, AIDW_E_INVALID_ARG, "GLOBAL bounds need robs_minmax");
+    } else if (nq > 0 && !robs_minmax && !h->ex_connected) {
+        return fail(h, AIDW_E_INVALID_ARG, "GLOBAL bounds need robs_minmax (or a connected bounds exchange)");
     }
     if (nq == 0) return AIDW_OK;
     if (!r_obs || !alpha) return fail(h, AIDW_E_INVALID_ARG, "r_obs/alpha is NULL");
     CK(h, cudaSetDevice(h->device));
+    // GLOBAL with robs_minmax == NULL on a connected handle: bounds from the exchange
+    const aidw::Scratch *ex = (rb == AIDW_RB_GLOBAL && !robs_minmax && h->ex_connected) ? h->sc : nullptr;
     return launched(h,
                     aidw::launch_alpha((int)h->dt, r_obs, nq, h->r_exp, alpha_lv, (int)rb, r_min, r_max,
-                                       robs_minmax, (int)mf, alpha, static_cast<cudaStream_t>(stream)),
+                                       robs_minmax, (int)mf, alpha, static_cast<cudaStream_t>(stream), ex),
                     "alpha kernel");
+}
+
+aidw_status aidw_exchange_setup(aidw_t h, int rank, int world, void *ipc_handle_out)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    if (world < 1 || world > aidw::kExMaxRanks || rank < 0 || rank >= world || !ipc_handle_out)
+        return fail(h, AIDW_E_INVALID_ARG, "rank %d / world %d (max %d) / handle buffer", rank, world,
+                    aidw::kExMaxRanks);
+    if (h->ex_own) return fail(h, AIDW_E_INVALID_ARG, "exchange already set up");
+    CK(h, cudaSetDevice(h->device));
+    cudaError_t e = cudaMalloc(&h->ex_own, sizeof(aidw::ExBuf));
+    if (e != cudaSuccess) {
+        h->ex_own = nullptr;
+        return cuda_fail(h, e, "cudaMalloc exchange buffer");
+    }
+    CK(h, cudaMemset(h->ex_own, 0, sizeof(aidw::ExBuf)));
+    cudaIpcMemHandle_t ih;
+    CK(h, cudaIpcGetMemHandle(&ih, h->ex_own));
+    std::memcpy(ipc_handle_out, &ih, sizeof ih);
+    h->ex_rank = rank;
+    h->ex_world = world;
+    return AIDW_OK;
+}
+
+aidw_status aidw_exchange_connect(aidw_t h, const void *ipc_handles)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    if (!h->ex_own || !ipc_handles) return fail(h, AIDW_E_INVALID_ARG, "aidw_exchange_setup first / NULL handles");
+    if (h->ex_connected) return fail(h, AIDW_E_INVALID_ARG, "exchange already connected");
+    CK(h, cudaSetDevice(h->device));
+    CK(h, cudaDeviceSynchronize());
+    const char *hb = static_cast<const char *>(ipc_handles);
+    aidw::ExBuf *ptrs[aidw::kExMaxRanks] = {};
+    for (int r = 0; r < h->ex_world; ++r) {
+        if (r == h->ex_rank) {
+            ptrs[r] = h->ex_own;
+            continue;
+        }
+        cudaIpcMemHandle_t ih;
+        std::memcpy(&ih, hb + (size_t)r * sizeof ih, sizeof ih);
+        void *p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return cuda_fail(h, e, "cudaIpcOpenMemHandle (peer exchange buffer)");
+        h->ex_mapped[r] = static_cast<aidw::ExBuf *>(p);
+        ptrs[r] = h->ex_mapped[r];
+    }
+    CK(h, cudaMalloc(&h->ex_peers_dev, sizeof(ptrs)));
+    CK(h, cudaMemcpy(h->ex_peers_dev, ptrs, sizeof(ptrs), cudaMemcpyHostToDevice));
+    aidw::Scratch sc;
+    CK(h, cudaMemcpy(&sc, h->sc, sizeof sc, cudaMemcpyDeviceToHost));
+    sc.ex_peers = h->ex_peers_dev;
+    sc.ex_rank = h->ex_rank;
+    sc.ex_world = h->ex_world;
+    sc.ex_epoch = 0;
+    sc.ex_timeout = 0;
+    CK(h, cudaMemcpy(h->sc, &sc, sizeof sc, cudaMemcpyHostToDevice));
+    h->ex_connected = true;
+    return AIDW_OK;
+}
+
+aidw_status aidw_exchange_close(aidw_t h)
+{
+    if (!h) return fail(nullptr, AIDW_E_INVALID_ARG, "handle is NULL");
+    CK(h, cudaSetDevice(h->device));
+    CK(h, cudaDeviceSynchronize());
+    if (h->ex_connected) {
+        aidw::Scratch sc;
+        CK(h, cudaMemcpy(&sc, h->sc, sizeof sc, cudaMemcpyDeviceToHost));
+        sc.ex_peers = nullptr;
+        sc.ex_world = 0;
+        CK(h, cudaMemcpy(h->sc, &sc, sizeof sc, cudaMemcpyHostToDevice));
+    }
+    for (int r = 0; r < aidw::kExMaxRanks; ++r)
+        if (h->ex_mapped[r]) {
+            cudaIpcCloseMemHandle(h->ex_mapped[r]);
+            h->ex_mapped[r] = nullptr;
+        }
+    if (h->ex_peers_dev) cudaFree(h->ex_peers_dev);
+    if (h->ex_own) cudaFree(h->ex_own);
+    h->ex_peers_dev = nullptr;
+    h->ex_own = nullptr;
+    h->ex_connected = false;
+    h->ex_world = 0;
+    h->ex_rank = -1;
+    return AIDW_OK;
 }
 
 aidw_status aidw_interpolate(aidw_t h, const void *qx, const void *qy, int64_t nq, const void *alpha,
@@ -569,6 +668,16 @@ aidw_status aidw_check(aidw_t h, void *stream)
         CK(h, cudaMemcpy(&h->sc->err_idx, &none, sizeof none, cudaMemcpyHostToDevice));
         return fail(h, AIDW_E_NONFINITE_INPUT, "non-finite query coordinate at query index %lld", idx);
     }
+    if (h->ex_connected) {
+        unsigned to = 0;
+        CK(h, cudaMemcpy(&to, &h->sc->ex_timeout, sizeof to, cudaMemcpyDeviceToHost));
+        if (to) {
+            const unsigned zero = 0;
+            CK(h, cudaMemcpy(&h->sc->ex_timeout, &zero, sizeof zero, cudaMemcpyHostToDevice));
+            return fail(h, AIDW_E_CUDA, "bounds exchange: a peer's {-min, max} did not arrive within ~2 s "
+                                        "(ranks out of step?); local bounds were used");
+        }
+    }
     return AIDW_OK;
 }
 
@@ -580,6 +689,7 @@ aidw_status aidw_run_host(aidw_t h, const void *qx_host, const void *qy_host, in
     if (nq < 0) return fail(h, AIDW_E_INVALID_ARG, "nq < 0");
     if (nq == 0) return AIDW_OK;
     if (!qx_host || !qy_host || !z_host) return fail(h, AIDW_E_INVALID_ARG, "NULL host buffer");
+    if (h->ex_connected) return fail(h, AIDW_E_INVALID_ARG, "aidw_run_host is single-rank; close the exchange first");
     aidw_status s = check_levels(h, alpha_lv);
     if (s != AIDW_OK) return s;
     if (rb == AIDW_RB_FIXED && !(r_min < r_max))
@@ -608,6 +718,7 @@ aidw_status aidw_destroy(aidw_t h)
 {
     if (!h) return AIDW_OK;
     cudaSetDevice(h->device);
+    if (h->ex_own || h->ex_connected) aidw_exchange_close(h);
     if (h->data || h->sc || h->work || h->filt.arrays || h->perm || h->split.p) cudaDeviceSynchronize();
     if (h->data) cudaFree(h->data);
     if (h->sc) cudaFree(h->sc);

@@ -39,6 +39,16 @@ struct SplitBuf {
     void *reserve(size_t n);
 };
 
+// Device-side GLOBAL-bounds exchange over peer memory (N4 push): every
+// rank owns one ExBuf; rank r's kNN epilogue writes its {-min, max} into val[r] of EVERY
+// rank's buffer (NVLink P2P stores through CUDA-IPC-mapped pointers) and then flag[r] =
+// epoch; the alpha kernel waits until all flags of its own buffer reach the epoch.
+constexpr int kExMaxRanks = 64;
+struct ExBuf {
+    unsigned long long flag[kExMaxRanks];
+    double val[kExMaxRanks][2];
+};
+
 // Device scratch owned by a handle.
 struct Scratch {
     unsigned long long mn;      // ordered bits of min r_obs (identity ~0ull)
@@ -49,6 +59,12 @@ struct Scratch {
     unsigned long long keys[4]; // bbox: ordered keys of min x, max x, min y, max y
     unsigned long long nonfinite;
     unsigned cls[8];            // weighting-pass class counts + cursors (launch_interp)
+    // bounds exchange (zero = off): peers[r] = rank r's ExBuf (device pointers)
+    ExBuf *const *ex_peers;
+    int ex_rank, ex_world;
+    unsigned long long ex_epoch;  // advanced by the kNN epilogue, read by the alpha kernel
+    unsigned ex_timeout;          // set when a wait gave up (reported by aidw_check)
+    unsigned pad1;
 };
 
 // Spatial (Morton) order of points and queries for the fp32 kNN:
@@ -105,7 +121,10 @@ int launch_minmax_identity(int dtype, void *minmax, cudaStream_t st);
 
 int launch_alpha(int dtype, const void *r_obs, int64_t nq, double r_exp, const double *lv,
                  int rb, double rmin, double rmax, const void *minmax, int mf, void *alpha,
-                 cudaStream_t st);
+                 cudaStream_t st, const Scratch *ex_sc = nullptr);
+
+// nq == 0 with an active exchange: push the MAX identity so peers do not wait.
+int launch_exchange_push_identity(Scratch *sc, cudaStream_t st);
 
 int launch_fused_fixed(const void *data, int64_t ndp, int64_t nd, FilterData *filt, const void *qx,
                        const void *qy, int64_t nq, int k, double r_exp, const double *lv, double rmin,

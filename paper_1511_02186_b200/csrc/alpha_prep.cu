@@ -106,14 +106,61 @@ int launch_prep(int dtype, int layout, const void *src, int64_t nd, int64_t ndp,
 // cy = y - c_y (RN), pp = fma(cx, cx, cy*cy); padding (+inf).
 // ------------------------------------------------------------------ S4: alpha
 // Eq. 4-6 per query in fp64 (passes.cuh alpha_eq); GLOBAL bounds read on the device.
+// GLOBAL bounds from the peer-memory exchange: thread 0 of each CTA
+// waits until every rank's flag in this rank's ExBuf reached the epoch the preceding kNN
+// epilogue published (acquire loads), then takes the MAX over ranks of {-min, max}.
+// Gives up after ~2 s (a missing peer) and flags ex_timeout for aidw_check.
+__device__ void exchange_wait(const Scratch *sc, double &v0, double &v1)
+{
+    __shared__ double s0, s1;
+    if (threadIdx.x == 0) {
+        const int n = sc->ex_world;
+        const unsigned long long ep = *reinterpret_cast<const volatile unsigned long long *>(&sc->ex_epoch);
+        const ExBuf *b = sc->ex_peers[sc->ex_rank];
+        const long long t0 = clock64();
+        bool ok = true;
+        for (int r = 0; r < n; ++r) {
+            unsigned long long f;
+            for (;;) {
+                asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(&b->flag[r]) : "memory");
+                if (f >= ep) break;
+                if (clock64() - t0 > 4000000000ll) {
+                    ok = false;
+                    break;
+                }
+                __nanosleep(100);
+            }
+            if (!ok) break;
+        }
+        if (!ok) atomicExch(const_cast<unsigned *>(&sc->ex_timeout), 1u);
+        double a0 = -__longlong_as_double(0x7ff0000000000000ll), a1 = a0;
+        for (int r = 0; r < n; ++r) {
+            a0 = fmax(a0, b->val[r][0]);
+            a1 = fmax(a1, b->val[r][1]);
+        }
+        s0 = a0;
+        s1 = a1;
+    }
+    __syncthreads();
+    v0 = s0;
+    v1 = s1;
+}
+
 template <typename T>
 __global__ void alpha_kernel(const T *__restrict__ robs, int64_t nq, double r_exp, Levels lv, int rb,
                              double rmin, double rmax, const T *__restrict__ mm, int mf,
-                             T *__restrict__ alpha)
+                             T *__restrict__ alpha, const Scratch *ex_sc)
 {
     if (rb == 0) {  // GLOBAL: bounds on r_obs -> bounds on R (division is monotone)
-        rmin = (double)(-mm[0]) / r_exp;
-        rmax = (double)mm[1] / r_exp;
+        double m0, m1;
+        if (ex_sc) {
+            exchange_wait(ex_sc, m0, m1);
+        } else {
+            m0 = (double)mm[0];
+            m1 = (double)mm[1];
+        }
+        rmin = -m0 / r_exp;
+        rmax = m1 / r_exp;
     }
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -121,7 +168,8 @@ __global__ void alpha_kernel(const T *__restrict__ robs, int64_t nq, double r_ex
 }
 
 int launch_alpha(int dtype, const void *r_obs, int64_t nq, double r_exp, const double *lvp, int rb,
-                 double rmin, double rmax, const void *minmax, int mf, void *alpha, cudaStream_t st)
+                 double rmin, double rmax, const void *minmax, int mf, void *alpha, cudaStream_t st,
+                 const Scratch *ex_sc)
 {
     Levels lv;
     for (int i = 0; i < 5; ++i) lv.a[i] = lvp[i];
@@ -130,11 +178,11 @@ int launch_alpha(int dtype, const void *r_obs, int64_t nq, double r_exp, const d
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (dtype == 0)
         alpha_kernel<float><<<(unsigned)blocks, threads, 0, st>>>(
-            (const float *)r_obs, nq, r_exp, lv, rb, rmin, rmax, (const float *)minmax, mf, (float *)alpha);
+            (const float *)r_obs, nq, r_exp, lv, rb, rmin, rmax, (const float *)minmax, mf, (float *)alpha, ex_sc);
     else
         alpha_kernel<double><<<(unsigned)blocks, threads, 0, st>>>(
             (const double *)r_obs, nq, r_exp, lv, rb, rmin, rmax, (const double *)minmax, mf,
-            (double *)alpha);
+            (double *)alpha, ex_sc);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -40,6 +40,34 @@ template <typename T> struct KnnArgs {
     const int *perm;  // nullable: launch slot i evaluates query perm[i] (spatial order, §4.7)
 };
 
+// Bounds exchange: values into val[rank] of every rank's ExBuf, a
+// system-scope fence, then the flags (release) -- P2P stores over NVLink.
+__device__ __forceinline__ void exchange_push(Scratch *sc, double v0, double v1)
+{
+    const unsigned long long ep = sc->ex_epoch + 1;
+    sc->ex_epoch = ep;
+    const int me = sc->ex_rank, n = sc->ex_world;
+    for (int r = 0; r < n; ++r) {
+        ExBuf *b = sc->ex_peers[r];
+        b->val[me][0] = v0;
+        b->val[me][1] = v1;
+    }
+    __threadfence_system();
+    for (int r = 0; r < n; ++r)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&sc->ex_peers[r]->flag[me]), "l"(ep) : "memory");
+}
+
+__global__ void exchange_push_identity_kernel(Scratch *sc)
+{
+    exchange_push(sc, -__longlong_as_double(0x7ff0000000000000ll), -__longlong_as_double(0x7ff0000000000000ll));
+}
+
+int launch_exchange_push_identity(Scratch *sc, cudaStream_t st)
+{
+    exchange_push_identity_kernel<<<1, 1, 0, st>>>(sc);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
 // Query index of launch slot `pos` (identity without a permutation).
 template <typename T> __device__ __forceinline__ int64_t query_of(const KnnArgs<T> &a, int64_t pos)
 {
@@ -174,6 +202,8 @@ __device__ __forceinline__ void knn_epilogue(const KnnArgs<T> &a, T (&buf)[Q][K]
                 a.sc->mx = 0ull;
                 a.sc->done = 0u;
                 __threadfence();
+                if (a.sc->ex_world > 0)  // N4 push: the bounds go straight to every peer
+                    exchange_push(a.sc, (double)a.minmax[0], (double)a.minmax[1]);
             }
         }
     }

@@ -42,12 +42,35 @@ def run_sharded(engine, qx, qy, k, levels, rbounds=GLOBAL, r_min=0.0, r_max=2.0,
     """Run S1..S5 on this rank's queries ``qx, qy`` with any engine exposing
     ``knn_robs(qx, qy, k) -> (r_obs, d1sq, minmax)``, ``alpha(...)`` and
     ``interpolate(...)`` (the CUDA :class:`~paper_1511_02186_b200.AIDW`; tests
-    inject a CPU engine to exercise this logic with gloo)."""
+    inject a CPU engine to exercise this logic with gloo).  An engine with a
+    connected device-side bounds exchange (:func:`connect_exchange`) needs no
+    host collective: its alpha kernel waits for the peers' pushed bounds."""
     r_obs, d1sq, mm = engine.knn_robs(qx, qy, k)
+    if rbounds == GLOBAL and getattr(engine, "exchanged", False):
+        a = engine.alpha(r_obs, levels, rbounds, r_min, r_max, None, muform)
+        return engine.interpolate(qx, qy, a, d1sq)
     if rbounds == GLOBAL and group is not None and dist.is_initialized():
         allreduce_bounds(mm, group)
     a = engine.alpha(r_obs, levels, rbounds, r_min, r_max, mm, muform)
     return engine.interpolate(qx, qy, a, d1sq)
+
+
+def connect_exchange(engine, group=None):
+    """Set up the device-side GLOBAL-bounds exchange (aidw_exchange_*):
+    every rank allocates its buffer, the 64-byte CUDA IPC handles are all-gathered
+    once over ``group`` (any backend), and each rank maps its peers' buffers.  After
+    this, every kNN launch pushes its bounds to all ranks from its last CTA and the
+    alpha kernel reads them on the device -- no collective per step."""
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    mine = engine.exchange_setup(rank, world)
+    handles = [None] * world
+    if world > 1:
+        dist.all_gather_object(handles, mine, group=group)
+    else:
+        handles = [mine]
+    engine.exchange_connect(handles)
+    return engine
 
 
 # ---------------------------------------------------------------------------------

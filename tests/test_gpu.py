@@ -6,6 +6,7 @@ precision (fp32 vs the oracle's float instantiation, fp64 vs fp64); Z within
 relative 1e-4 (fp32) / 1e-10 (fp64) of the fp64 oracle.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -349,6 +350,46 @@ def test_graph_replay_bit_identical(P, dtype, nq):
         ze, te = eng.run(qx2, qy2, 10, LV, P.GLOBAL, trace=True)
         assert torch.equal(zg, ze)
         assert torch.equal(g.r_obs, te["r_obs"]) and torch.equal(g.alpha, te["alpha"])
+
+
+@pytest.mark.parametrize("split", ["even", "empty_rank"])
+def test_bounds_exchange_two_processes(P, tmp_path, split):
+    """N4 device-initiated min/max push (aidw_exchange_*): 2 processes on one GPU map
+    each other's exchange buffers (CUDA IPC), every kNN epilogue pushes its {-min, max}
+    and the alpha kernel waits for the peer on the device; Z is bit-identical to a
+    single-process run over all queries (MAX is exact).  'empty_rank': one rank has no
+    queries and pushes the MAX identity."""
+    import torch.multiprocessing as mp
+    x, y, z, qx, qy = datagen.random_cloud(4242, 60000, 50000)
+    ref = P.AIDW(x, y, z).run(qx, qy, 10, LV, P.GLOBAL).cpu().numpy()
+    cut = [0, 20000, 50000] if split == "even" else [0, 0, 50000]
+    port = 29600 + (os.getpid() % 200)
+    from exchange_worker import run as worker
+    mp.start_processes(worker, args=(2, port, cut, str(tmp_path)), nprocs=2, join=True, start_method="spawn")
+    zs = [np.load(tmp_path / f"z{r}.npy") for r in range(2)]
+    for step in range(3):
+        got = np.concatenate([zs[0][step], zs[1][step]])
+        assert np.array_equal(got, ref), step
+
+
+def test_bounds_exchange_single_rank(P):
+    """world = 1: the exchange degenerates to a self-push; results equal the plain path,
+    also through a captured CUDA graph (the epoch advances on the device)."""
+    x, y, z, qx, qy = datagen.random_cloud(77, 30000, 9000)
+    eng = P.AIDW(x, y, z)
+    ref = eng.run(qx, qy, 10, LV, P.GLOBAL).cpu().numpy()
+    eng.exchange_connect([eng.exchange_setup(0, 1)])
+    for _ in range(2):
+        assert np.array_equal(eng.run(qx, qy, 10, LV, P.GLOBAL).cpu().numpy(), ref)
+    g = eng.capture(len(qx), 10, LV, P.GLOBAL)
+    for _ in range(2):
+        assert np.array_equal(g.replay(qx, qy).cpu().numpy(), ref)
+    eng.check()
+    with pytest.raises(P.AidwError, match="robs_minmax"):
+        P.aidw_knn_robs(eng.h, torch.as_tensor(qx, device="cuda"), torch.as_tensor(qy, device="cuda"), 10,
+                        torch.empty(len(qx), device="cuda"))
+    eng.exchange_close()
+    assert np.array_equal(eng.run(qx, qy, 10, LV, P.GLOBAL).cpu().numpy(), ref)
 
 
 def test_errors(P):
