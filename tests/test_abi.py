@@ -69,6 +69,10 @@ def test_argument_errors_without_gpu(pkg):
     assert L.aidw_knn_robs(None, None, None, 0, 10, None, None, None, None, None) == 1
     assert L.aidw_destroy(None) == 0
     assert L.aidw_launch_count(None) == -1
+    # bounds exchange entry points (device push, N4): NULL handle
+    assert L.aidw_exchange_setup(None, 0, 2, ctypes.create_string_buffer(64)) == 1
+    assert L.aidw_exchange_connect(None, None) == 1
+    assert L.aidw_exchange_close(None) == 1
 
 
 def test_no_cpu_fallback(pkg, monkeypatch):
