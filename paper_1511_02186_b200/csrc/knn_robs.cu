@@ -406,12 +406,17 @@ static int launch_knn_filter_t(KnnArgs<float> a, const FilterArgs &f, cudaStream
     if (set_filter_attrs<K, Q, G, false, MINB>(smem) < 0) return -1;
     const int64_t per_cta = (int64_t)kBlock * Q;
     const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
-    const int S =
-        knn_split_factor((const void *)knn_filter_kernel<K, Q, G, false, MINB>, smem, grid, (int)(a.ndp / kTileKF), a, sp);
+    // A spatially ordered batch is never split: a split scans in the caller's order and
+    // restarts every split's top-k warm-up, which costs more than the idle SMs it fills
+    // (C3, 400 CTAs on 888 slots: 3.25 ms split x2 vs 1.76 ms ordered).
+    const bool ordered = fd && fd->cell_start && order_queries(a.nq);
+    const int S = ordered ? (a.lists = nullptr, 1)
+                          : knn_split_factor((const void *)knn_filter_kernel<K, Q, G, false, MINB>, smem, grid,
+                                             (int)(a.ndp / kTileKF), a, sp);
     int pre = 0;
     if (S == 1) {
         FilterArgs fo = f;
-        if (fd && fd->cell_start && order_queries(a.nq)) {
+        if (ordered) {
             pre = launch_order_queries(a.qx, a.qy, a.nq, fd, &fd->qorder, &a.perm, st);
             if (pre < 0) return -1;
             if (a.perm) {  // Morton-ordered copy of the data
