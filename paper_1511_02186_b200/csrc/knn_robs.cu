@@ -23,6 +23,7 @@
 #include "passes.cuh"
 
 #include <climits>
+#include <cmath>
 #include <cstdlib>
 
 namespace aidw {
@@ -303,25 +304,40 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
                       reinterpret_cast<uint64_t *>(spy + STAGES * TILE) + STAGES};
     const int nt_all = (int)(a.ndp / TILE);
     const TileRange tr = SPLIT ? split_range(nt_all) : TileRange{0, nt_all};
-    const int ntiles = tr.nloc;
-    // Spatial order (§4.7): the CTA's queries are neighbours, so it starts its scan at the
-    // (Morton-sorted) data tile under its middle query and wraps around -- the top-k is
-    // near-final after the first tiles and the filter then rejects almost every group.
-    int start = 0;
-    if (!SPLIT && a.perm) {
+    // Spatial order (§4.7): the CTA's queries are neighbours.  Its "home" tile is the
+    // (Morton-sorted) data tile under its middle query.  Unsplit, the scan starts there
+    // and wraps around, so the top-k is near-final after the first tiles and the filter
+    // then rejects almost every group.  Split (seeded, §4.6), the CTA first scans the home
+    // tile only to SEED its lists: the k-th smallest s over those k real points is an
+    // upper bound of the query's true k-th distance, and filling the list with copies of
+    // it (instead of +inf) lets the split's own range start filtered.  The merged
+    // multiset is unchanged: every point below the seed is still inserted by the split
+    // that owns it, and a seed copy survives the merge only where the true k-th distance
+    // equals the seed value.
+    int home = 0;
+    if (a.perm) {
         const int64_t mid = min((int64_t)blockIdx.x * (kBlock * Q) + kBlock * Q / 2, a.nq - 1);
         const int64_t qm = a.perm[mid];
-        start = f.cell_start[morton_cell(a.qx[qm], a.qy[qm], f.grid)] / TILE - 1;
-        start = start < 0 ? start + nt_all : (start >= nt_all ? nt_all - 1 : start);
+        home = (int)(f.cell_start[morton_cell(a.qx[qm], a.qy[qm], f.grid)] / TILE);
+        home = home >= nt_all ? nt_all - 1 : home;
     }
+    const bool seed = SPLIT && a.perm != nullptr;
+    int start = 0;
+    if (!SPLIT && a.perm) start = home == 0 ? nt_all - 1 : home - 1;
+    const int ntiles = tr.nloc + (seed ? 1 : 0);
     if (threadIdx.x == 0) ring.init();
     __syncthreads();
 
     auto issue = [&](int tile, int slot) {
         constexpr uint32_t B = TILE * sizeof(float);
         mbar_arrive_expect_tx(&ring.full[slot], 5u * B);
-        int pt = tr.t0 + tile + start;
-        pt = pt >= nt_all ? pt - nt_all : pt;
+        int pt;
+        if (SPLIT) {
+            pt = seed ? (tile == 0 ? home : tr.t0 + tile - 1) : tr.t0 + tile;
+        } else {
+            pt = tile + start;
+            pt = pt >= nt_all ? pt - nt_all : pt;
+        }
         const int64_t off = (int64_t)pt * TILE;
         bulk_g2s(scx + slot * TILE, f.cx + off, B, &ring.full[slot]);
         bulk_g2s(scy + slot * TILE, f.cy + off, B, &ring.full[slot]);
@@ -346,6 +362,7 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
         ring.wait_full(t);
         const int o = ring.slot(t) * TILE;
         knn_f32_tile<K, Q, G, TILE>(st, scx + o, scy + o, spp + o, spx + o, spy + o);
+        if (seed && t == 0) st.seed_lists(k0);  // home tile scanned: lists := seed copies
         ring.release(t, ntiles, issue);
     }
     if constexpr (SPLIT)
@@ -366,6 +383,45 @@ static int knn_split_factor(const void *kern, size_t smem, unsigned grid, int nt
     a.lists = nullptr;
     if (!sp) return 1;
     const int S = choose_split(kern, kBlock, smem, grid, ntiles, 1);
+    if (S <= 1) return 1;
+    a.lists = static_cast<T *>(sp->reserve((size_t)S * (size_t)a.nq * (size_t)a.k * sizeof(T)));
+    return a.lists ? S : 1;
+}
+
+// Seeded split of a spatially ordered batch: the factor S <= 8 minimising the waves per
+// split, ceil(grid S / slots) / S, with each split's extra seed tile counted
+// (C4: 2,000 CTAs on 592 slots -> S = 5, 17 waves of 1/5 instead of 4 of 1).
+// AIDW_SPLIT=0 disables, AIDW_SPLIT=n forces n (tests).
+template <typename T>
+static int ordered_split_factor(const void *kern, size_t smem, unsigned grid, int ntiles, KnnArgs<T> &a, SplitBuf *sp)
+{
+    a.lists = nullptr;
+    if (!sp) return 1;
+    int S = 1;
+    const char *e = getenv("AIDW_SPLIT");  // read per launch so tests can toggle it
+    const int forced = e ? atoi(e) : -1;
+    if (forced == 0) return 1;
+    if (forced > 0) {
+        S = forced < 8 ? forced : 8;
+    } else {
+        int dev = 0, sms = 148, occ = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, smem) != cudaSuccess) {
+            cudaGetLastError();
+            return 1;
+        }
+        const double slots = (double)occ * sms;
+        double best = 0.0;
+        for (int s = 1; s <= 8 && ntiles / s >= 8; ++s) {
+            const double waves = std::ceil((double)grid * s / slots);
+            const double cost = waves / s * (1.0 + (double)s / ntiles);
+            if (s == 1 || cost < best * 0.995) {
+                best = cost;
+                S = s;
+            }
+        }
+    }
     if (S <= 1) return 1;
     a.lists = static_cast<T *>(sp->reserve((size_t)S * (size_t)a.nq * (size_t)a.k * sizeof(T)));
     return a.lists ? S : 1;
@@ -406,32 +462,34 @@ static int launch_knn_filter_t(KnnArgs<float> a, const FilterArgs &f, cudaStream
     if (set_filter_attrs<K, Q, G, false, MINB>(smem) < 0) return -1;
     const int64_t per_cta = (int64_t)kBlock * Q;
     const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
-    // A spatially ordered batch is never split: a split scans in the caller's order and
-    // restarts every split's top-k warm-up, which costs more than the idle SMs it fills
-    // (C3, 400 CTAs on 888 slots: 3.25 ms split x2 vs 1.76 ms ordered).
+    // A spatially ordered batch splits only with seeded lists (knn_filter_kernel), by the
+    // factor that best fills the last wave (ordered_split_factor); an unordered one by
+    // whole extra waves (knn_split_factor: its splits restart the top-k warm-up).
     const bool ordered = fd && fd->cell_start && order_queries(a.nq);
-    const int S = ordered ? (a.lists = nullptr, 1)
+    if (ordered && set_filter_attrs<K, Q, G, true, MINB>(smem) < 0) return -1;
+    const int S = ordered ? ordered_split_factor((const void *)knn_filter_kernel<K, Q, G, true, MINB>, smem, grid,
+                                                 (int)(a.ndp / kTileKF), a, sp)
                           : knn_split_factor((const void *)knn_filter_kernel<K, Q, G, false, MINB>, smem, grid,
                                              (int)(a.ndp / kTileKF), a, sp);
     int pre = 0;
-    if (S == 1) {
-        FilterArgs fo = f;
-        if (ordered) {
-            pre = launch_order_queries(a.qx, a.qy, a.nq, fd, &fd->qorder, &a.perm, st);
-            if (pre < 0) return -1;
-            if (a.perm) {  // Morton-ordered copy of the data
-                const float *c = static_cast<const float *>(fd->arrays);
-                fo.cx = c + 3 * a.ndp;
-                fo.cy = c + 4 * a.ndp;
-                fo.pp = c + 5 * a.ndp;
-                fo.px = c + 6 * a.ndp;
-                fo.py = c + 7 * a.ndp;
-            }
+    FilterArgs fo = f;
+    if (ordered) {
+        pre = launch_order_queries(a.qx, a.qy, a.nq, fd, &fd->qorder, &a.perm, st);
+        if (pre < 0) return -1;
+        if (a.perm) {  // Morton-ordered copy of the data
+            const float *c = static_cast<const float *>(fd->arrays);
+            fo.cx = c + 3 * a.ndp;
+            fo.cy = c + 4 * a.ndp;
+            fo.pp = c + 5 * a.ndp;
+            fo.px = c + 6 * a.ndp;
+            fo.py = c + 7 * a.ndp;
         }
+    }
+    if (S == 1) {
         knn_filter_kernel<K, Q, G, false, MINB><<<grid, kBlock, smem, st>>>(a, fo);
     } else {
         if (set_filter_attrs<K, Q, G, true, MINB>(smem) < 0) return -1;
-        knn_filter_kernel<K, Q, G, true, MINB><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, f);
+        knn_filter_kernel<K, Q, G, true, MINB><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, fo);
     }
     const int n = knn_finish(a, S, st);
     return n < 0 ? -1 : n + pre;

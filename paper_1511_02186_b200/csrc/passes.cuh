@@ -132,6 +132,19 @@ struct KnnF32State {
 #pragma unroll
         for (int i = 0; i < K; ++i) buf[q][i] = (i < k0) ? -pos_inf<float>() : pos_inf<float>();
     }
+    // Seeded split (knn_filter_kernel): replace each list by k copies of its current
+    // k-th value v (an upper bound of the query's k-th distance when the list holds k
+    // real points; +inf otherwise) and filter against it.
+    __device__ __forceinline__ void seed_lists(int k0)
+    {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const float v = buf[q][K - 1];
+#pragma unroll
+            for (int i = 0; i < K; ++i) buf[q][i] = (i < k0) ? -pos_inf<float>() : v;
+            thr[q] = thr_of(v, qqf[q], mf[q], Ef[q]);
+        }
+    }
 };
 
 // Filter values t = pp + A cx + B cy of the 8 points at tile offset j for query q, as

@@ -319,17 +319,24 @@ def test_knn_order_bit_identical(P, orc, monkeypatch, case):
             qx[::5], qy[::5] = x[: len(qx[::5])], y[: len(qy[::5])]
     eng = P.AIDW(x, y, z)
     res = {}
-    for sv in ("0", None):
-        if sv is None:
+    # (order, split): unordered; ordered with the default (seeded) split; ordered unsplit;
+    # ordered with forced seeded splits 2 and 7
+    for sv in ("0", None, "s0", "s2", "s7"):
+        monkeypatch.delenv("AIDW_SPLIT", raising=False)
+        if sv is None or sv.startswith("s"):
             monkeypatch.delenv("AIDW_KNN_ORDER", raising=False)
+            if sv:
+                monkeypatch.setenv("AIDW_SPLIT", sv[1:])
         else:
             monkeypatch.setenv("AIDW_KNN_ORDER", sv)
         r, d1, mm, dd = eng.knn_robs(qx, qy, k, want_dists=True)
         zr = eng.run(qx, qy, k, LV, P.GLOBAL)
         zf, tf = eng.run_fixed(qx, qy, k, LV, 0.0, 2.0, trace=True)  # N1 fused kernel, same order
         res[sv] = [t.cpu().numpy() for t in (r, d1, mm, dd, zr, zf, tf["r_obs"], tf["alpha"])]
-    for n, (u, v) in enumerate(zip(res[None], res["0"])):
-        assert np.array_equal(u, v), n
+    monkeypatch.delenv("AIDW_SPLIT", raising=False)
+    for sv in (None, "s0", "s2", "s7"):
+        for n, (u, v) in enumerate(zip(res[sv], res["0"])):
+            assert np.array_equal(u, v), (sv, n)
     idx = np.random.default_rng(5).choice(len(qx), 300, replace=False)
     ro = orc.knn_f32(x, y, qx[idx], qy[idx], k)
     assert np.array_equal(res[None][0][idx], ro)
