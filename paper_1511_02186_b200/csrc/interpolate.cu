@@ -34,8 +34,8 @@ template <typename T> struct InterpArgs {
 // Weight math per precision: fp32 MUFU (scalar variant), fp64 table + polynomial
 // (passes.cuh log2_f64 / exp2_f64; tables staged in shared memory).
 struct F64Tabs {
-    double2 lg[64];
-    double ex[16];
+    double2 lg[1 << kLog2TabBits];
+    double ex[1 << kExp2TabBits];
 };
 __device__ __forceinline__ float wlog2(float s, const F64Tabs &) { return lg2_approx(s); }
 __device__ __forceinline__ double wlog2(double s, const F64Tabs &t) { return log2_f64(s, t.lg); }
@@ -83,8 +83,9 @@ __global__ void __launch_bounds__(kBlock) interp_kernel(const InterpArgs<T> a)
     const int t0 = block_tile(b0, ntiles_all, nblk), ntiles = block_tile(b1, ntiles_all, nblk) - t0;
     if (threadIdx.x == 0) r.ring.init();
     if (sizeof(T) == 8) {
-        if (threadIdx.x < 64) tabs.lg[threadIdx.x] = make_double2(kLog2Tab[threadIdx.x][0], kLog2Tab[threadIdx.x][1]);
-        if (threadIdx.x < 16) tabs.ex[threadIdx.x] = kExp2Tab[threadIdx.x];
+        for (int i = threadIdx.x; i < (1 << kLog2TabBits); i += blockDim.x)
+            tabs.lg[i] = make_double2(kLog2Tab[i][0], kLog2Tab[i][1]);
+        for (int i = threadIdx.x; i < (1 << kExp2TabBits); i += blockDim.x) tabs.ex[i] = kExp2Tab[i];
     }
     __syncthreads();
     auto issue = [&](int tile, int slot) { r.issue(a, t0 + tile, slot); };

@@ -256,21 +256,22 @@ __device__ __forceinline__ void knn_f32_tile(KnnF32State<K, Q> &st, const float 
 // The fp64 weighting pass needs w to ~1e-12 relative (Z tolerance 1e-10), far below
 // libdevice's cost (~90 FP64 ops per pair for log2 + exp2).  Both use a small table in
 // shared memory (tools/gen_f64_tables.py) and a short Taylor polynomial:
-//  log2(s) = e + LOGM[i] + log2(1 + t),  t = m * C[i] - 1, |t| <= 0.0078, degree 6
-//            (truncation 3.5e-16); valid for normal s > 0.
-//  exp2(x) = 2^j * T[k] * 2^r,  16x = 16j + k + 16r rounded, |r| <= 1/32, degree 7
-//            (truncation < 1e-17); x clamped to >= -1000 (smaller weights vanish).
+//  log2(s) = e + LOGM[i] + log2(1 + t),  t = m * C[i] - 1, i = top 8 mantissa bits,
+//            |t| <= 2^-9, degree 5 (truncation 1.3e-17); valid for normal s > 0.
+//  exp2(x) = 2^j * T[k] * 2^r,  64x = 64j + k + 64r rounded, |r| <= 1/128, degree 5
+//            (truncation < 4e-17); x clamped to >= -1000 (smaller weights vanish).
+// (v11: 256/64-entry tables instead of 64/16 save 4 of ~29 FP64 ops per pair.)
 __device__ __forceinline__ double log2_f64(double s, const double2 *__restrict__ tab)
 {
     const unsigned long long bits = (unsigned long long)__double_as_longlong(s);
     const unsigned be = (unsigned)(bits >> 52) & 0x7ffu;
-    const int i = (int)(bits >> 46) & 63;
+    const int i = (int)(bits >> (52 - kLog2TabBits)) & ((1 << kLog2TabBits) - 1);
     const double m = __longlong_as_double((long long)((bits & 0x000fffffffffffffull) | 0x3ff0000000000000ull));
     const double2 ci = tab[i];
     const double t = fma(m, ci.x, -1.0);
-    double p = kLog2Poly[6];
+    double p = kLog2Poly[4];
 #pragma unroll
-    for (int k = 5; k >= 0; --k) p = fma(p, t, kLog2Poly[k]);
+    for (int k = 3; k >= 0; --k) p = fma(p, t, kLog2Poly[k]);
     // exponent as double without a conversion: 2^52 + be, minus (2^52 + 1023)
     const double ed = __longlong_as_double((long long)(0x4330000000000000ull | be)) - (4503599627370496.0 + 1023.0);
     return ed + fma(p, t, ci.y);
@@ -280,16 +281,17 @@ __device__ __forceinline__ double exp2_f64(double x, const double *__restrict__ 
 {
     constexpr double kM = 6755399441055744.0;  // 1.5 * 2^52
     x = fmax(x, -1000.0);
-    const double t = fma(x, 16.0, kM);
+    constexpr double kN = (double)(1 << kExp2TabBits);
+    const double t = fma(x, kN, kM);
     const double nd = t - kM;
-    const double r = fma(nd, -0.0625, x);
+    const double r = fma(nd, -1.0 / kN, x);
     const int n = (int)(unsigned)(unsigned long long)__double_as_longlong(t);
-    double p = kExp2Poly[7];
+    double p = kExp2Poly[5];
 #pragma unroll
-    for (int k = 6; k >= 0; --k) p = fma(p, r, kExp2Poly[k]);
-    const double y = tab[n & 15] * p;
-    // multiply by 2^(n >> 4) through the exponent field (no overflow: y <= 2, n <= 0)
-    return __longlong_as_double(__double_as_longlong(y) + ((long long)(n >> 4) << 52));
+    for (int k = 4; k >= 0; --k) p = fma(p, r, kExp2Poly[k]);
+    const double y = tab[n & ((1 << kExp2TabBits) - 1)] * p;
+    // multiply by 2^(n >> bits) through the exponent field (no overflow: y <= 2, n <= 0)
+    return __longlong_as_double(__double_as_longlong(y) + ((long long)(n >> kExp2TabBits) << 52));
 }
 
 // ------------------------------------------------------------------ Eq. 4-6
