@@ -290,26 +290,33 @@ aidw_status aidw_create(aidw_t *out, int device, aidw_dtype dt, aidw_layout lay,
                          x1, y0, y1));
     h->r_exp = 1.0 / (2.0 * std::sqrt((double)nd / h->area));  // Eq. 2, printed order
 
-    if (dt == AIDW_F32) {
-        // centred filter arrays for the fp32 kNN; c = bbox centre in fp32,
-        // r1 >= max |x - c_x| + |y - c_y| over the data (fp64, padded for fp32 rounding)
+    {
+        // centred filter arrays for the kNN; c = bbox centre in fp32,
+        // r1 >= max |x - c_x| + |y - c_y| over the data (fp64, padded for fp32 rounding).
+        // fp64 handles use the same fp32 filter (fp64 re-check) when the data extent keeps
+        // the filter arithmetic in fp32's normal range: R1 in [2^-60, 2^60].
         const char *env = getenv("AIDW_KNN_FILTER");
-        if (!(env && env[0] == '0')) {
+        const float cxf = (float)(0.5 * (x0 + x1)), cyf = (float)(0.5 * (y0 + y1));
+        const double rx = std::fmax(std::fabs(x0 - cxf), std::fabs(x1 - cxf));
+        const double ry = std::fmax(std::fabs(y0 - cyf), std::fabs(y1 - cyf));
+        const double r1 = (rx + ry) * (1.0 + 1e-6);
+        const bool safe = dt == AIDW_F32 || (std::isfinite(cxf) && std::isfinite(cyf) && r1 >= 0x1p-60 && r1 <= 0x1p60);
+        if (!(env && env[0] == '0') && safe) {
             if ((e = cudaMalloc(&h->filt.arrays, 8 * (size_t)h->ndp * sizeof(float))) != cudaSuccess ||
-                (e = cudaMalloc(&h->filt.cell_start, (aidw::kCells + 1) * sizeof(int))) != cudaSuccess) {
+                (e = cudaMalloc(&h->filt.cell_start, (aidw::kCells + 1) * sizeof(int))) != cudaSuccess ||
+                (dt == AIDW_F64 &&
+                 (e = cudaMalloc(&h->filt.coords64, 2 * (size_t)h->ndp * sizeof(double))) != cudaSuccess)) {
                 cudaGetLastError();
                 return bail(fail(h, AIDW_E_NOMEM, "cudaMalloc filter: %s", cudaGetErrorString(e)));
             }
-            h->filt.c_x = (float)(0.5 * (x0 + x1));
-            h->filt.c_y = (float)(0.5 * (y0 + y1));
-            const double rx = std::fmax(std::fabs(x0 - h->filt.c_x), std::fabs(x1 - h->filt.c_x));
-            const double ry = std::fmax(std::fabs(y0 - h->filt.c_y), std::fabs(y1 - h->filt.c_y));
-            h->filt.r1 = (float)((rx + ry) * (1.0 + 1e-6));
+            h->filt.c_x = cxf;
+            h->filt.c_y = cyf;
+            h->filt.r1 = (float)r1;
             // Morton order grid over the data bbox
             constexpr double cells = (double)(1 << aidw::kOrderBits);
             h->filt.grid = aidw::OrderGrid{(float)x0, (float)y0, (float)(cells / (x1 - x0)),
                                            (float)(cells / (y1 - y0))};
-            s = launched(h, aidw::launch_order_data(h->data, h->ndp, nd, &h->filt, st), "order data kernels");
+            s = launched(h, aidw::launch_order_data((int)dt, h->data, h->ndp, nd, &h->filt, st), "order data kernels");
             if (s != AIDW_OK) return bail(s);
             if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return bail(cuda_fail(h, e, "order data sync"));
         }
@@ -725,6 +732,7 @@ aidw_status aidw_destroy(aidw_t h)
     if (h->work) cudaFree(h->work);
     if (h->filt.arrays) cudaFree(h->filt.arrays);
     if (h->filt.cell_start) cudaFree(h->filt.cell_start);
+    if (h->filt.coords64) cudaFree(h->filt.coords64);
     if (h->filt.qorder.p) cudaFree(h->filt.qorder.p);
     if (h->perm) cudaFree(h->perm);
     if (h->split.p) cudaFree(h->split.p);

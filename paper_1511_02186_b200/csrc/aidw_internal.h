@@ -91,6 +91,7 @@ __host__ __device__ inline unsigned morton_cell(float x, float y, OrderGrid g)
 // sorted position.
 struct FilterData {
     void *arrays = nullptr;
+    double *coords64 = nullptr;  // fp64 handles: [2][ndp] x, y in Morton order (re-check)
     float c_x = 0.f, c_y = 0.f, r1 = 0.f;
     int *cell_start = nullptr;  // [kCells + 1]
     OrderGrid grid{0.f, 0.f, 0.f, 0.f};
@@ -99,7 +100,9 @@ struct FilterData {
 
 // Morton-sort the data into the filter arrays (3 launches) and order a query batch
 // (perm[i] = query of launch slot i; 3 launches + a memset; scratch from `buf`).
-int launch_order_data(const void *data, int64_t ndp, int64_t nd, FilterData *fd, cudaStream_t st);
+int launch_order_data(int dtype, const void *data, int64_t ndp, int64_t nd, FilterData *fd, cudaStream_t st);
+int launch_order_queries(const double *qx, const double *qy, int64_t nq, const FilterData *fd, SplitBuf *buf,
+                         const int **perm, cudaStream_t st);
 int launch_order_queries(const float *qx, const float *qy, int64_t nq, const FilterData *fd, SplitBuf *buf,
                          const int **perm, cudaStream_t st);
 

@@ -180,7 +180,7 @@ int launch_fused_fixed(const void *data, int64_t ndp, int64_t nd, FilterData *fi
     a.pz = p + 2 * ndp;
     a.ndp = ndp;
     a.nd = nd;
-    a.f = FilterArgs{c, c + ndp, c + 2 * ndp, p, p + ndp, filt->c_x, filt->c_y, filt->r1, filt->cell_start,
+    a.f = FilterArgs{c, c + ndp, c + 2 * ndp, p, p + ndp, nullptr, nullptr, filt->c_x, filt->c_y, filt->r1, filt->cell_start,
                      filt->grid};  // caller's order
     a.qx = (const float *)qx;
     a.qy = (const float *)qy;

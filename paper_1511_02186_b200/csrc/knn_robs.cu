@@ -287,21 +287,26 @@ __global__ void __launch_bounds__(kBlock) knn_robs_kernel(const KnnArgs<T> a)
 }
 
 // ---------------------------------------------------------------------------------
-// Filtered fp32 kernel (passes.cuh knn_f32_tile): smem tiles of (cx, cy, pp, x, y).
+// Filtered kernel (passes.cuh knn_f32_tile): smem tiles of the fp32 filter arrays
+// (cx, cy, pp) and -- fp32 -- the coordinates (x, y) for the canonical re-check; fp64
+// handles re-check from the global fp64 coordinates (rare path only) and keep their
+// top-k in fp64.
 // MINB = 0: no occupancy hint (an explicit minBlocks of 1 lets ptxas use up to 255
 // registers and was measured slower: 113 vs 108 ms at C4).
-template <int K, int Q, int G, bool SPLIT, int MINB = 0>
-__global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<float> a, const FilterArgs f)
+template <typename T> __host__ __device__ constexpr int filter_arrays() { return sizeof(T) == 4 ? 5 : 3; }
+
+template <typename T, int K, int Q, int G, bool SPLIT, int MINB = 0>
+__global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<T> a, const FilterArgs f)
 {
-    constexpr int TILE = kTileKF, STAGES = kStagesKF;
+    constexpr int TILE = kTileKF, STAGES = kStagesKF, NARR = filter_arrays<T>();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float *scx = reinterpret_cast<float *>(smem_raw);
     float *scy = scx + STAGES * TILE;
     float *spp = scy + STAGES * TILE;
-    float *spx = spp + STAGES * TILE;
+    float *spx = spp + STAGES * TILE;  // fp32 only
     float *spy = spx + STAGES * TILE;
-    Ring<STAGES> ring{reinterpret_cast<uint64_t *>(spy + STAGES * TILE),
-                      reinterpret_cast<uint64_t *>(spy + STAGES * TILE) + STAGES};
+    Ring<STAGES> ring{reinterpret_cast<uint64_t *>(scx + NARR * STAGES * TILE),
+                      reinterpret_cast<uint64_t *>(scx + NARR * STAGES * TILE) + STAGES};
     const int nt_all = (int)(a.ndp / TILE);
     const TileRange tr = SPLIT ? split_range(nt_all) : TileRange{0, nt_all};
     // Spatial order (§4.7): the CTA's queries are neighbours.  Its "home" tile is the
@@ -318,57 +323,62 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
     if (a.perm) {
         const int64_t mid = min((int64_t)blockIdx.x * (kBlock * Q) + kBlock * Q / 2, a.nq - 1);
         const int64_t qm = a.perm[mid];
-        home = (int)(f.cell_start[morton_cell(a.qx[qm], a.qy[qm], f.grid)] / TILE);
+        home = (int)(f.cell_start[morton_cell((float)a.qx[qm], (float)a.qy[qm], f.grid)] / TILE);
         home = home >= nt_all ? nt_all - 1 : home;
     }
     const bool seed = SPLIT && a.perm != nullptr;
     int start = 0;
     if (!SPLIT && a.perm) start = home == 0 ? nt_all - 1 : home - 1;
     const int ntiles = tr.nloc + (seed ? 1 : 0);
+    auto tile_of = [&](int tile) {  // global tile index of ring tile `tile`
+        if (SPLIT) return seed ? (tile == 0 ? home : tr.t0 + tile - 1) : tr.t0 + tile;
+        const int pt = tile + start;
+        return pt >= nt_all ? pt - nt_all : pt;
+    };
     if (threadIdx.x == 0) ring.init();
     __syncthreads();
 
     auto issue = [&](int tile, int slot) {
         constexpr uint32_t B = TILE * sizeof(float);
-        mbar_arrive_expect_tx(&ring.full[slot], 5u * B);
-        int pt;
-        if (SPLIT) {
-            pt = seed ? (tile == 0 ? home : tr.t0 + tile - 1) : tr.t0 + tile;
-        } else {
-            pt = tile + start;
-            pt = pt >= nt_all ? pt - nt_all : pt;
-        }
-        const int64_t off = (int64_t)pt * TILE;
+        mbar_arrive_expect_tx(&ring.full[slot], (uint32_t)NARR * B);
+        const int64_t off = (int64_t)tile_of(tile) * TILE;
         bulk_g2s(scx + slot * TILE, f.cx + off, B, &ring.full[slot]);
         bulk_g2s(scy + slot * TILE, f.cy + off, B, &ring.full[slot]);
         bulk_g2s(spp + slot * TILE, f.pp + off, B, &ring.full[slot]);
-        bulk_g2s(spx + slot * TILE, f.px + off, B, &ring.full[slot]);
-        bulk_g2s(spy + slot * TILE, f.py + off, B, &ring.full[slot]);
+        if constexpr (NARR == 5) {
+            bulk_g2s(spx + slot * TILE, f.px + off, B, &ring.full[slot]);
+            bulk_g2s(spy + slot * TILE, f.py + off, B, &ring.full[slot]);
+        }
     };
     if (threadIdx.x == 0)
         for (int s = 0; s < STAGES && s < ntiles; ++s) issue(s, s);
 
     const int64_t base = (int64_t)blockIdx.x * (kBlock * Q) + threadIdx.x;
-    float qx[Q], qy[Q];
+    T qx[Q], qy[Q];
     bool valid[Q];
     int64_t qid[Q];
-    load_queries<float, Q>(a, base, qx, qy, valid, qid);
+    load_queries<T, Q>(a, base, qx, qy, valid, qid);
     const int k0 = K - a.k;
-    KnnF32State<K, Q> st;
+    KnnF32State<K, Q, T> st;
 #pragma unroll
     for (int q = 0; q < Q; ++q) st.init(q, qx[q], qy[q], f, k0);
 
     for (int t = 0; t < ntiles; ++t) {
         ring.wait_full(t);
         const int o = ring.slot(t) * TILE;
-        knn_f32_tile<K, Q, G, TILE>(st, scx + o, scy + o, spp + o, spx + o, spy + o);
+        if constexpr (NARR == 5) {
+            knn_f32_tile<K, Q, G, TILE>(st, scx + o, scy + o, spp + o, spx + o, spy + o);
+        } else {
+            const int64_t off = (int64_t)tile_of(t) * TILE;
+            knn_f32_tile<K, Q, G, TILE, T>(st, scx + o, scy + o, spp + o, f.px64 + off, f.py64 + off);
+        }
         if (seed && t == 0) st.seed_lists(k0);  // home tile scanned: lists := seed copies
         ring.release(t, ntiles, issue);
     }
     if constexpr (SPLIT)
-        knn_write_split<float, K, Q>(a, st.buf, valid, qid, k0);
+        knn_write_split<T, K, Q>(a, st.buf, valid, qid, k0);
     else
-        knn_epilogue<float, K, Q>(a, st.buf, valid, qid, k0);
+        knn_epilogue<T, K, Q>(a, st.buf, valid, qid, k0);
 }
 
 // ---------------------------------------------------------------------------------
@@ -436,9 +446,9 @@ template <typename T> static int knn_finish(const KnnArgs<T> &a, int S, cudaStre
 }
 
 // ---------------------------------------------------------------------------------
-template <int K, int Q, int G, bool SPLIT, int MINB> static int set_filter_attrs(size_t smem)
+template <typename T, int K, int Q, int G, bool SPLIT, int MINB> static int set_filter_attrs(size_t smem)
 {
-    auto kern = knn_filter_kernel<K, Q, G, SPLIT, MINB>;
+    auto kern = knn_filter_kernel<T, K, Q, G, SPLIT, MINB>;
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
                    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) == cudaSuccess
                ? 0
@@ -454,22 +464,23 @@ static bool order_queries(int64_t nq)
     return nq >= kOrderMinQ && nq <= INT_MAX && !(e && e[0] == '0');  // perm is int32
 }
 
-template <int K, int Q, int G = 8, int MINB = 0>
-static int launch_knn_filter_t(KnnArgs<float> a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp,
+template <int K, int Q, int G = 8, int MINB = 0, typename T = float>
+static int launch_knn_filter_t(KnnArgs<T> a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp,
                                FilterData *fd)
 {
-    const size_t smem = (size_t)5 * kStagesKF * kTileKF * sizeof(float) + 2 * kStagesKF * sizeof(uint64_t);
-    if (set_filter_attrs<K, Q, G, false, MINB>(smem) < 0) return -1;
+    const size_t smem =
+        (size_t)filter_arrays<T>() * kStagesKF * kTileKF * sizeof(float) + 2 * kStagesKF * sizeof(uint64_t);
+    if (set_filter_attrs<T, K, Q, G, false, MINB>(smem) < 0) return -1;
     const int64_t per_cta = (int64_t)kBlock * Q;
     const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
     // A spatially ordered batch splits only with seeded lists (knn_filter_kernel), by the
     // factor that best fills the last wave (ordered_split_factor); an unordered one by
     // whole extra waves (knn_split_factor: its splits restart the top-k warm-up).
     const bool ordered = fd && fd->cell_start && order_queries(a.nq);
-    if (ordered && set_filter_attrs<K, Q, G, true, MINB>(smem) < 0) return -1;
-    const int S = ordered ? ordered_split_factor((const void *)knn_filter_kernel<K, Q, G, true, MINB>, smem, grid,
-                                                 (int)(a.ndp / kTileKF), a, sp)
-                          : knn_split_factor((const void *)knn_filter_kernel<K, Q, G, false, MINB>, smem, grid,
+    if (ordered && set_filter_attrs<T, K, Q, G, true, MINB>(smem) < 0) return -1;
+    const int S = ordered ? ordered_split_factor((const void *)knn_filter_kernel<T, K, Q, G, true, MINB>, smem,
+                                                 grid, (int)(a.ndp / kTileKF), a, sp)
+                          : knn_split_factor((const void *)knn_filter_kernel<T, K, Q, G, false, MINB>, smem, grid,
                                              (int)(a.ndp / kTileKF), a, sp);
     int pre = 0;
     FilterArgs fo = f;
@@ -483,13 +494,17 @@ static int launch_knn_filter_t(KnnArgs<float> a, const FilterArgs &f, cudaStream
             fo.pp = c + 5 * a.ndp;
             fo.px = c + 6 * a.ndp;
             fo.py = c + 7 * a.ndp;
+            if (fd->coords64) {  // fp64 handles: the sorted fp64 coordinates for the re-check
+                fo.px64 = fd->coords64;
+                fo.py64 = fd->coords64 + a.ndp;
+            }
         }
     }
     if (S == 1) {
-        knn_filter_kernel<K, Q, G, false, MINB><<<grid, kBlock, smem, st>>>(a, fo);
+        knn_filter_kernel<T, K, Q, G, false, MINB><<<grid, kBlock, smem, st>>>(a, fo);
     } else {
-        if (set_filter_attrs<K, Q, G, true, MINB>(smem) < 0) return -1;
-        knn_filter_kernel<K, Q, G, true, MINB><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, fo);
+        if (set_filter_attrs<T, K, Q, G, true, MINB>(smem) < 0) return -1;
+        knn_filter_kernel<T, K, Q, G, true, MINB><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, fo);
     }
     const int n = knn_finish(a, S, st);
     return n < 0 ? -1 : n + pre;
@@ -503,6 +518,24 @@ static int knn_variant()
         v = e ? atoi(e) : 0;
     }
     return v;
+}
+
+// fp64 handles: the same fp32 filter, fp64 re-check and top-k (Q = 2, G = 16 for every K;
+// the fp64 lists take twice the registers).
+static int dispatch_filter_k(const KnnArgs<double> &a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp,
+                             FilterData *fd)
+{
+    const int k = a.k;
+    if (k <= 1) return launch_knn_filter_t<1, 2, 16, 0, double>(a, f, st, sp, fd);
+    if (k <= 2) return launch_knn_filter_t<2, 2, 16, 0, double>(a, f, st, sp, fd);
+    if (k <= 4) return launch_knn_filter_t<4, 2, 16, 0, double>(a, f, st, sp, fd);
+    if (k <= 8) return launch_knn_filter_t<8, 2, 16, 0, double>(a, f, st, sp, fd);
+    if (k <= 10) return launch_knn_filter_t<10, 2, 16, 0, double>(a, f, st, sp, fd);
+    if (k <= 12) return launch_knn_filter_t<12, 2, 16, 0, double>(a, f, st, sp, fd);
+    if (k <= 15) return launch_knn_filter_t<15, 2, 16, 0, double>(a, f, st, sp, fd);
+    if (k <= 16) return launch_knn_filter_t<16, 2, 16, 0, double>(a, f, st, sp, fd);
+    if (k <= 24) return launch_knn_filter_t<24, 1, 16, 0, double>(a, f, st, sp, fd);
+    return launch_knn_filter_t<32, 1, 16, 0, double>(a, f, st, sp, fd);
 }
 
 static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp,
@@ -664,8 +697,8 @@ int launch_knn(int dtype, int k, const void *data, int64_t ndp, const void *qx, 
             const float *c = static_cast<const float *>(filt->arrays);
             // caller's order (unordered launches); the Morton-ordered copy is selected in
             // launch_knn_filter_t when the query batch is ordered (§4.7)
-            FilterArgs f{c, c + ndp, c + 2 * ndp, p, p + ndp, filt->c_x, filt->c_y, filt->r1, filt->cell_start,
-                         filt->grid};
+            FilterArgs f{c, c + ndp, c + 2 * ndp, p, p + ndp, nullptr, nullptr, filt->c_x, filt->c_y, filt->r1,
+                         filt->cell_start, filt->grid};
             return dispatch_filter_k(a, f, st, sp, filt);
         }
         return dispatch_k(a, st, sp);
@@ -673,6 +706,12 @@ int launch_knn(int dtype, int k, const void *data, int64_t ndp, const void *qx, 
     const double *p = static_cast<const double *>(data);
     KnnArgs<double> a{p, p + ndp, ndp, (const double *)qx, (const double *)qy, nq, k,
                       (double *)r_obs, (double *)d1sq, (double *)minmax, (double *)dists, sc, dists_sq, nullptr, nullptr};
+    if (filt && filt->arrays) {  // fp32 filter, fp64 re-check from the handle's data (caller's order)
+        const float *c = static_cast<const float *>(filt->arrays);
+        FilterArgs f{c, c + ndp, c + 2 * ndp, nullptr, nullptr, p, p + ndp, filt->c_x, filt->c_y, filt->r1,
+                     filt->cell_start, filt->grid};
+        return dispatch_filter_k(a, f, st, sp, filt);
+    }
     return dispatch_k(a, st, sp);
 }
 

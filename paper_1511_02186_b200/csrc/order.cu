@@ -20,11 +20,13 @@ namespace aidw {
 
 namespace {
 
-__global__ void cell_hist_kernel(const float *__restrict__ x, const float *__restrict__ y, int64_t n, OrderGrid g,
+// (fp64 coordinates pick their cell in fp32: any order is valid, only its cost changes)
+template <typename T>
+__global__ void cell_hist_kernel(const T *__restrict__ x, const T *__restrict__ y, int64_t n, OrderGrid g,
                                  unsigned *__restrict__ counts)
 {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(&counts[morton_cell(x[i], y[i], g)], 1u);
+        atomicAdd(&counts[morton_cell((float)x[i], (float)y[i], g)], 1u);
 }
 
 // Exclusive scan of kCells counts by one CTA of 32 warps: warp w owns the contiguous
@@ -84,36 +86,48 @@ __global__ void __launch_bounds__(kScanThreads) cell_scan_kernel(const unsigned 
 }
 
 // Data: the centred filter values in the caller's order (for unordered launches) and,
-// with the coordinates, at sorted positions; padding slots [nd, ndp) get +inf.
-__global__ void order_data_scatter_kernel(const float *__restrict__ px, const float *__restrict__ py, int64_t nd,
+// with the coordinates, at sorted positions; padding slots [nd, ndp) get +inf.  fp64
+// data: the centred values are the fp64 differences rounded once to fp32 (passes.cuh
+// centre_f32), and the fp64 coordinates are also written in sorted order (s64).
+__device__ __forceinline__ float centre_d(float x, float c) { return __fsub_rn(x, c); }
+__device__ __forceinline__ float centre_d(double x, float c) { return __double2float_rn(x - (double)c); }
+
+template <typename T>
+__global__ void order_data_scatter_kernel(const T *__restrict__ px, const T *__restrict__ py, int64_t nd,
                                           int64_t ndp, OrderGrid g, float c_x, float c_y,
-                                          int *__restrict__ cursor, float *__restrict__ out)
+                                          int *__restrict__ cursor, float *__restrict__ out, double *__restrict__ s64)
 {
     float *ux = out, *uy = out + ndp, *up = out + 2 * ndp;  // caller's order
     float *cx = out + 3 * ndp, *cy = out + 4 * ndp, *pp = out + 5 * ndp, *sx = out + 6 * ndp, *sy = out + 7 * ndp;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndp;
          i += (int64_t)gridDim.x * blockDim.x) {
         if (i < nd) {
-            const float x = px[i], y = py[i];
-            const int64_t o = atomicAdd(&cursor[morton_cell(x, y, g)], 1);
-            const float a = __fsub_rn(x, c_x), b = __fsub_rn(y, c_y);
+            const T x = px[i], y = py[i];
+            const int64_t o = atomicAdd(&cursor[morton_cell((float)x, (float)y, g)], 1);
+            const float a = centre_d(x, c_x), b = centre_d(y, c_y);
             const float p2 = __fmaf_rn(a, a, __fmul_rn(b, b));
             ux[i] = cx[o] = a;
             uy[i] = cy[o] = b;
             up[i] = pp[o] = p2;
-            sx[o] = x;
-            sy[o] = y;
+            sx[o] = (float)x;
+            sy[o] = (float)y;
+            if (s64) {
+                s64[o] = (double)x;
+                s64[ndp + o] = (double)y;
+            }
         } else {
             ux[i] = uy[i] = up[i] = cx[i] = cy[i] = pp[i] = sx[i] = sy[i] = pos_inf<float>();
+            if (s64) s64[i] = s64[ndp + i] = pos_inf<double>();
         }
     }
 }
 
-__global__ void order_query_scatter_kernel(const float *__restrict__ qx, const float *__restrict__ qy, int64_t nq,
+template <typename T>
+__global__ void order_query_scatter_kernel(const T *__restrict__ qx, const T *__restrict__ qy, int64_t nq,
                                            OrderGrid g, int *__restrict__ cursor, int *__restrict__ perm)
 {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x)
-        perm[atomicAdd(&cursor[morton_cell(qx[i], qy[i], g)], 1)] = (int)i;
+        perm[atomicAdd(&cursor[morton_cell((float)qx[i], (float)qy[i], g)], 1)] = (int)i;
 }
 
 unsigned grid_for(int64_t n)
@@ -125,27 +139,34 @@ unsigned grid_for(int64_t n)
 
 }  // namespace
 
-int launch_order_data(const void *data, int64_t ndp, int64_t nd, FilterData *fd, cudaStream_t st)
+template <typename T> static int order_data_t(const T *px, int64_t ndp, int64_t nd, FilterData *fd, cudaStream_t st)
 {
-    const float *px = static_cast<const float *>(data), *py = px + ndp;
+    const T *py = px + ndp;
     unsigned *counts = nullptr;
     int *cursor = nullptr;
     if (cudaMallocAsync(&counts, kCells * sizeof(unsigned), st) != cudaSuccess ||
         cudaMallocAsync(&cursor, kCells * sizeof(int), st) != cudaSuccess ||
         cudaMemsetAsync(counts, 0, kCells * sizeof(unsigned), st) != cudaSuccess)
         return -1;
-    cell_hist_kernel<<<grid_for(nd), 256, 0, st>>>(px, py, nd, fd->grid, counts);
+    cell_hist_kernel<T><<<grid_for(nd), 256, 0, st>>>(px, py, nd, fd->grid, counts);
     cell_scan_kernel<<<1, kScanThreads, 0, st>>>(counts, fd->cell_start, cursor);
-    order_data_scatter_kernel<<<grid_for(ndp), 256, 0, st>>>(px, py, nd, ndp, fd->grid, fd->c_x, fd->c_y, cursor,
-                                                             static_cast<float *>(fd->arrays));
+    order_data_scatter_kernel<T><<<grid_for(ndp), 256, 0, st>>>(px, py, nd, ndp, fd->grid, fd->c_x, fd->c_y, cursor,
+                                                                static_cast<float *>(fd->arrays), fd->coords64);
     const bool ok = cudaPeekAtLastError() == cudaSuccess;
     cudaFreeAsync(counts, st);
     cudaFreeAsync(cursor, st);
     return ok ? 3 : -1;
 }
 
-int launch_order_queries(const float *qx, const float *qy, int64_t nq, const FilterData *fd, SplitBuf *buf,
-                         const int **perm, cudaStream_t st)
+int launch_order_data(int dtype, const void *data, int64_t ndp, int64_t nd, FilterData *fd, cudaStream_t st)
+{
+    return dtype == 0 ? order_data_t(static_cast<const float *>(data), ndp, nd, fd, st)
+                      : order_data_t(static_cast<const double *>(data), ndp, nd, fd, st);
+}
+
+template <typename T>
+static int order_queries_t(const T *qx, const T *qy, int64_t nq, const FilterData *fd, SplitBuf *buf,
+                           const int **perm, cudaStream_t st)
 {
     // buf layout: counts [kCells] | start [kCells + 1] | cursor [kCells] | perm [nq]
     const size_t head = (size_t)(3 * kCells + 1) * sizeof(int);
@@ -156,12 +177,24 @@ int launch_order_queries(const float *qx, const float *qy, int64_t nq, const Fil
     int *cursor = start + kCells + 1;
     int *p = cursor + kCells;
     if (cudaMemsetAsync(counts, 0, kCells * sizeof(unsigned), st) != cudaSuccess) return -1;
-    cell_hist_kernel<<<grid_for(nq), 256, 0, st>>>(qx, qy, nq, fd->grid, counts);
+    cell_hist_kernel<T><<<grid_for(nq), 256, 0, st>>>(qx, qy, nq, fd->grid, counts);
     cell_scan_kernel<<<1, kScanThreads, 0, st>>>(counts, start, cursor);
-    order_query_scatter_kernel<<<grid_for(nq), 256, 0, st>>>(qx, qy, nq, fd->grid, cursor, p);
+    order_query_scatter_kernel<T><<<grid_for(nq), 256, 0, st>>>(qx, qy, nq, fd->grid, cursor, p);
     if (cudaPeekAtLastError() != cudaSuccess) return -1;
     *perm = p;
     return 3;
+}
+
+int launch_order_queries(const float *qx, const float *qy, int64_t nq, const FilterData *fd, SplitBuf *buf,
+                         const int **perm, cudaStream_t st)
+{
+    return order_queries_t(qx, qy, nq, fd, buf, perm, st);
+}
+
+int launch_order_queries(const double *qx, const double *qy, int64_t nq, const FilterData *fd, SplitBuf *buf,
+                         const int **perm, cudaStream_t st)
+{
+    return order_queries_t(qx, qy, nq, fd, buf, perm, st);
 }
 
 }  // namespace aidw

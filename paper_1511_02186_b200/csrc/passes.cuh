@@ -89,7 +89,8 @@ __device__ __forceinline__ void robs_of(const T (&b)[K], int k0, int k, T &robs,
 //   + 8u(n1+R1)^2; the constants below double every term.
 struct FilterArgs {
     const float *cx, *cy, *pp;  // centred filter arrays, padded with +inf (spatial order)
-    const float *px, *py;       // the same points' coordinates (canonical re-check)
+    const float *px, *py;       // the same points' coordinates (canonical re-check, fp32)
+    const double *px64, *py64;  // fp64 handles: the same points' fp64 coordinates (global)
     float c_x, c_y;             // centre
     float r1;                   // R1 bound
     const int *cell_start;      // first sorted position of each Morton cell (§4.7)
@@ -109,28 +110,43 @@ __device__ __forceinline__ float thr_of(float thr, float qq, float m, float E)
     return __fmaf_ru(0x1p-21f, r2 + qq + E, v);
 }
 
-// Per-thread state of the filtered kNN for Q queries.
-template <int K, int Q>
-struct KnnF32State {
-    float qx[Q], qy[Q], thr[Q], qqf[Q], mf[Q], Ef[Q], A[Q], B[Q];
-    float buf[Q][K];
+// Centred query coordinate in fp32: one rounding of q - c (fp32 queries: __fsub_rn; fp64
+// queries: the fp64 difference rounded to fp32 -- relative error u(1 + 2^-29), inside the
+// factor-2 slack of the centring term m).
+__device__ __forceinline__ float centre_f32(float x, float c) { return __fsub_rn(x, c); }
+__device__ __forceinline__ float centre_f32(double x, float c) { return __double2float_rn(x - (double)c); }
+// The k-th canonical distance on the filter's fp32 scale, rounded up (fp64: s64 < thr64
+// <= thr32 and the fp64 canonical s is within 4u64 << 4u of the exact distance, so the
+// fp32 margin of thr_of covers it).
+__device__ __forceinline__ float thr_f32(float v) { return v; }
+__device__ __forceinline__ float thr_f32(double v) { return __double2float_ru(v); }
 
-    __device__ __forceinline__ void init(int q, float x, float y, const FilterArgs &f, int k0)
+// Per-thread state of the filtered kNN for Q queries; T = working precision of the
+// queries, the canonical re-check and the top-k (the filter itself is always fp32).
+template <int K, int Q, typename T = float>
+struct KnnF32State {
+    T qx[Q], qy[Q];
+    float thr[Q], qqf[Q], mf[Q], Ef[Q], A[Q], B[Q];
+    T buf[Q][K];
+
+    __device__ __forceinline__ void init(int q, T x, T y, const FilterArgs &f, int k0)
     {
         qx[q] = x;
         qy[q] = y;
-        const float qcx = __fsub_rn(x, f.c_x), qcy = __fsub_rn(y, f.c_y);
+        float qcx = centre_f32(x, f.c_x), qcy = centre_f32(y, f.c_y);
+        const double u = 0x1p-24;
+        double qq = (double)qcx * (double)qcx + (double)qcy * (double)qcy;
+        const double n1r = fabs((double)qcx) + fabs((double)qcy) + (double)f.r1;
+        const bool ok = n1r <= 0x1p60;  // else (far outside the fp32-safe range, or NaN)
+        if (!ok) qcx = qcy = 0.f, qq = 0.0;  // unfiltered: t = pp <= +inf = thr for every point
         A[q] = opaque(-2.0f * qcx);  // opaque: keep in a register, never re-derived per group
         B[q] = opaque(-2.0f * qcy);
         thr[q] = pos_inf<float>();
-        const double u = 0x1p-24;
-        const double qq = (double)qcx * (double)qcx + (double)qcy * (double)qcy;
-        const double n1r = fabs((double)qcx) + fabs((double)qcy) + (double)f.r1;
         qqf[q] = __double2float_ru(qq);
-        mf[q] = __double2float_ru(8.0 * u * n1r);
-        Ef[q] = __double2float_ru(16.0 * u * n1r * n1r + 6.0 * u * qq);
+        mf[q] = ok ? __double2float_ru(8.0 * u * n1r) : pos_inf<float>();  // m = +inf keeps thr at +inf
+        Ef[q] = ok ? __double2float_ru(16.0 * u * n1r * n1r + 6.0 * u * qq) : 0.f;
 #pragma unroll
-        for (int i = 0; i < K; ++i) buf[q][i] = (i < k0) ? -pos_inf<float>() : pos_inf<float>();
+        for (int i = 0; i < K; ++i) buf[q][i] = (i < k0) ? -pos_inf<T>() : pos_inf<T>();
     }
     // Seeded split (knn_filter_kernel): replace each list by k copies of its current
     // k-th value v (an upper bound of the query's k-th distance when the list holds k
@@ -139,18 +155,18 @@ struct KnnF32State {
     {
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            const float v = buf[q][K - 1];
+            const T v = buf[q][K - 1];
 #pragma unroll
-            for (int i = 0; i < K; ++i) buf[q][i] = (i < k0) ? -pos_inf<float>() : v;
-            thr[q] = thr_of(v, qqf[q], mf[q], Ef[q]);
+            for (int i = 0; i < K; ++i) buf[q][i] = (i < k0) ? -pos_inf<T>() : v;
+            thr[q] = thr_of(thr_f32(v), qqf[q], mf[q], Ef[q]);
         }
     }
 };
 
 // Filter values t = pp + A cx + B cy of the 8 points at tile offset j for query q, as
 // four packed couples (2 FFMA2 each).
-template <int K, int Q>
-__device__ __forceinline__ void filter8(const KnnF32State<K, Q> &st, int q, const float *__restrict__ tcx,
+template <int K, int Q, typename T>
+__device__ __forceinline__ void filter8(const KnnF32State<K, Q, T> &st, int q, const float *__restrict__ tcx,
                                         const float *__restrict__ tcy, const float *__restrict__ tpp, int j,
                                         float (&t)[8])
 {
@@ -173,10 +189,12 @@ __device__ __forceinline__ void filter8(const KnnF32State<K, Q> &st, int q, cons
 // the smem loads shared by the Q queries); a group that passes for some lane re-derives
 // its t values in the rare path, builds the bitmask of passing pairs and re-checks only
 // those with the canonical distance.
-template <int K, int Q, int G, int TILE>
-__device__ __forceinline__ void knn_f32_tile(KnnF32State<K, Q> &st, const float *__restrict__ tcx,
+// tpx, tpy: the tile's original coordinates for the canonical re-check -- the smem tile
+// (fp32) or the global fp64 arrays at the tile's offset (fp64; read only in the rare path).
+template <int K, int Q, int G, int TILE, typename T = float>
+__device__ __forceinline__ void knn_f32_tile(KnnF32State<K, Q, T> &st, const float *__restrict__ tcx,
                                              const float *__restrict__ tcy, const float *__restrict__ tpp,
-                                             const float *__restrict__ tpx, const float *__restrict__ tpy)
+                                             const T *__restrict__ tpx, const T *__restrict__ tpy)
 {
     static_assert(G % 8 == 0 && G <= 32 && TILE % G == 0, "group size");
     const uint32_t acx = smem_addr(tcx), acy = smem_addr(tcy), app = smem_addr(tpp);
@@ -237,16 +255,16 @@ __device__ __forceinline__ void knn_f32_tile(KnnF32State<K, Q> &st, const float 
                     if (mask) {
                         const int e = __ffs(mask) - 1;
                         mask &= mask - 1;
-                        const float s = dist_sq(st.qx[q], st.qy[q], tpx[j + e], tpy[j + e]);
+                        const T s = dist_sq(st.qx[q], st.qy[q], tpx[j + e], tpy[j + e]);
                         if (s < st.buf[q][K - 1]) {
-                            topk_insert<float, K>(st.buf[q], s);
+                            topk_insert<T, K>(st.buf[q], s);
                             inserted = true;
                         }
                     }
                 }
                 // one threshold update per group (candidates of this group were all
                 // checked exactly against the current k-th distance above)
-                if (inserted) st.thr[q] = thr_of(st.buf[q][K - 1], st.qqf[q], st.mf[q], st.Ef[q]);
+                if (inserted) st.thr[q] = thr_of(thr_f32(st.buf[q][K - 1]), st.qqf[q], st.mf[q], st.Ef[q]);
             }
         }
     }

@@ -595,3 +595,39 @@ def test_knn_filter_translated_scaled(P, orc, offset, scale):
     Zg = eng.run(qx, qy, 10, LV, P.GLOBAL).cpu().numpy()
     Zo = orc.aidw(x, y, z, qx, qy, 10, LV, mode="global")
     assert rel_err(Zg, Zo).max() <= 1e-4
+
+
+@pytest.mark.parametrize("offset,scale,nq", [(0.0, 1.0, 900), (1.0e6, 1.0e-3, 900), (-3.0e4, 1.0e12, 900),
+                                             (0.25, 2.0 ** -50, 900), (0.0, 2.0 ** -70, 900), (7.0, 1.0, 40000)])
+def test_knn_filter_f64(P, orc, monkeypatch, offset, scale, nq):
+    """fp64 handles share the fp32 filter with an fp64 canonical re-check:
+    on fp64 inputs that fp32 cannot represent, translated and scaled (2^-70: the data
+    extent leaves the fp32-safe range and the filter is off), unordered and spatially
+    ordered (40,000 queries, seeded split), the k distances are bit-identical to the
+    unfiltered fp64 kernel and within 1e-15 of the fp64 oracle; queries far outside the
+    data (|q - c| > 2^60, unfiltered per query) included."""
+    rng = np.random.default_rng(404)
+    x, y = rng.random(6000), rng.random(6000)
+    z = 1.0 + rng.random(6000)
+    qx, qy = rng.random(nq) * 1.2 - 0.1, rng.random(nq) * 1.2 - 0.1
+    x[1::5], y[1::5] = x[::5][: len(x[1::5])], y[::5][: len(y[1::5])]  # duplicates
+    qx[::7], qy[::7] = x[: len(qx[::7])], y[: len(qy[::7])]  # queries on data points
+    f = lambda v: offset + scale * v
+    x, y, qx, qy = f(x), f(y), f(qx), f(qy)
+    if scale == 1.0:
+        qx[3] = 1.0e70  # far field: per-query unfiltered
+    res = {}
+    for flt in ("1", "0"):
+        monkeypatch.setenv("AIDW_KNN_FILTER", flt)  # read at handle creation
+        eng = P.AIDW(x, y, z, dtype=torch.float64)
+        res[flt] = gpu_knn(P, eng, qx, qy, 10)
+        eng.close()
+    for u, v in zip(res["1"], res["0"]):
+        assert np.array_equal(u, v)
+    # the oracle evaluates Eq. 1's distance as written (dx*dx + dy*dy, two roundings) and
+    # the kernels the canonical fma sequence (R16): equal on grid inputs, within an ulp
+    # or two here
+    idx = np.arange(0, nq, max(1, nq // 300))
+    ro, do = orc.knn_f64(x, y, qx[idx], qy[idx], 10, want_dists=True)
+    np.testing.assert_allclose(res["1"][3][idx], do, rtol=1e-15, atol=0)
+    np.testing.assert_allclose(res["1"][0][idx], ro, rtol=1e-15, atol=0)
