@@ -36,8 +36,10 @@
  *    AIDW_SPLIT=0|n (data split off / forced factor) and AIDW_KNN_ORDER=0 (no
  *    spatial query order) are read per call; AIDW_ALPHA_CLASSES=0 (no
  *    exact-exponent weighting classes) and AIDW_KNN_VARIANT / AIDW_INTERP_VARIANT
- *    (tuning sweeps) once per process; AIDW_KNN_FILTER=0 (canonical fp32 kNN) at
- *    aidw_create.
+ *    (tuning sweeps) once per process; AIDW_KNN_FILTER=0 (canonical kNN, no fp32
+ *    filter, for either dtype) at aidw_create.  Spatially ordered kNN batches
+ *    (>= 32768 queries) split the data range only with seeded lists (DESIGN.md
+ *    §4.6); AIDW_SPLIT=n forces that factor (at most 8) too.
  */
 #ifndef AIDW_H
 #define AIDW_H
@@ -132,6 +134,10 @@ AIDW_API aidw_dtype aidw_dtype_of(aidw_t h);
  * (Eq. 3), summed in ascending order.
  * Distance arithmetic (R16), in T with round-to-nearest:
  *   dx = qx - px; dy = qy - py; s = fma(dx, dx, dy*dy); selection on s; d = sqrt(s).
+ * (Both dtypes skip most pairs' canonical evaluation through an fp32 expanded-form
+ * filter with a rigorous rounding margin; every pair that could enter the top-k is
+ * re-evaluated with the sequence above, so the selected multiset is exactly the
+ * unfiltered one -- DESIGN.md §4.1.)
  *   qx, qy      : device T[nq]
  *   k           : 1..AIDW_KMAX, nd >= k (else AIDW_E_INSUFFICIENT_DATA)
  *   r_obs       : device T[nq] out
@@ -166,7 +172,8 @@ AIDW_API aidw_status aidw_alpha(aidw_t h, const void *r_obs, int64_t nq, const d
  * w_i = d_i^-alpha (Eq. 1; all points).
  * Evaluated as w_i = 2^(-alpha/2 * log2(s_i / d1sq)) (scaled by the nearest
  * distance, which cancels in Eq. 1).  fp32: MUFU lg2/ex2, sums in fp32 within
- * 512-point tiles and fp64 across tiles; fp64: libdevice log2/exp2, fp64 sums.
+ * 512-point tiles and fp64 across tiles; fp64: table + Taylor log2/exp2 (relative
+ * error < 1e-15), fp64 sums.
  * Exact coincidence (d1sq == 0): Z = mean of z over the data points at distance 0
  * (R19).
  *   qx, qy : device T[nq];  alpha : device T[nq] (from aidw_alpha)
