@@ -571,7 +571,17 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
         return launch_knn_filter_t<10, 2, 16>(a, f, st, sp, fd);
     }
     if (k <= 12) return launch_knn_filter_t<12, 2, 16>(a, f, st, sp, fd);
-    if (k <= 15) return launch_knn_filter_t<15, 2, 16>(a, f, st, sp, fd);
+    if (k > 12 && k <= 15) {
+        switch (knn_variant()) {  // tuning sweep at C3 (tools/tune_knn.py, TUNE_CFG=C3)
+        case 16: return launch_knn_filter_t<15, 4, 32>(a, f, st, sp, fd);
+        case 17: return launch_knn_filter_t<15, 2, 32>(a, f, st, sp, fd);
+        case 18: return launch_knn_filter_t<15, 1, 32>(a, f, st, sp, fd);
+        case 19: return launch_knn_filter_t<15, 2, 8>(a, f, st, sp, fd);
+        case 20: return launch_knn_filter_t<15, 1, 16>(a, f, st, sp, fd);
+        default: break;
+        }
+    }
+    if (k <= 15) return launch_knn_filter_t<15, 2, 32>(a, f, st, sp, fd);  // C3: 1.95 vs 2.03 ms (G = 16)
     if (k <= 16) return launch_knn_filter_t<16, 2, 16>(a, f, st, sp, fd);
     if (k <= 24) return launch_knn_filter_t<24, 2>(a, f, st, sp, fd);
     return launch_knn_filter_t<32, 2>(a, f, st, sp, fd);
