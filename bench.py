@@ -48,6 +48,13 @@ MUFU_PER_CLK_SM = 15.96   # measured MUFU.EX2/LG2 per SM per clock
 FMA_PER_CLK_SM = 123.2    # measured FFMA2 (packed) FMA ops per SM per clock
 KNN_FP32_PER_PAIR = 4     # canonical kNN distance (2 sub, mul, fma) -- SIMT FP32 bound
 N_SM = 148
+# fp64 (--dtype f64): the weighting pass has no hardware transcendental;
+# per pair it issues 25 FP64 instructions (distance 4, table + degree-5 log2 ~9, exponent
+# 1, table + degree-5 exp2 ~9, sums 2; counted on the ncu source page,
+# profiles/r01_ncu_interp_f64_v12.json) on the FP64 pipe; DFMA rate measured by
+# tools/pipe_peaks.cu (profiles/r01_pipe_peaks.json).
+DP_PER_PAIR = 25
+DFMA_PER_CLK_SM = 64.0
 
 
 def weight_clk_per_pair(fp32=WEIGHT_FP32_PER_PAIR, transc=TRANSC_PER_PAIR):
@@ -202,13 +209,14 @@ def run_reference(args):
     return 0
 
 
-def workload_name(n, nq=NQ_PER_GPU, mode="global"):
+def workload_name(n, nq=NQ_PER_GPU, mode="global", dtype="f32"):
     rb = {"global": "GLOBAL R bounds", "fixed": "FIXED R bounds (0, 2), fused kernel",
           "fixed3": "FIXED R bounds (0, 2), stage kernels"}[mode]
+    prec = "fp64" if dtype == "f64" else "fp32"
     if n == 1:
-        tag = "C4" if nq == NQ_PER_GPU else "C4-shaped"
-        return f"{tag}: 1,024,000 data x {nq:,} queries, k=10, fp32, uniform, {rb}"
-    return (f"C4 weak-scaled: 1,024,000 data x {n}x{nq:,} queries ({nq} per GPU), k=10, fp32, "
+        tag = ("C4" if nq == NQ_PER_GPU else "C4-shaped") + (" (fp64)" if dtype == "f64" else "")
+        return f"{tag}: 1,024,000 data x {nq:,} queries, k=10, {prec}, uniform, {rb}"
+    return (f"C4 weak-scaled: 1,024,000 data x {n}x{nq:,} queries ({nq} per GPU), k=10, {prec}, "
             f"uniform, {rb}" + (f" allreduced over {n} GPUs" if mode == "global" else ""))
 
 
@@ -226,6 +234,8 @@ def main():
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
                     help="GLOBAL bounds: NCCL allreduce(MAX) (default) or the device-side push over "
                          "peer memory (aidw_exchange_*, no collective per step)")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"],
+                    help="working precision of the path (f64: the fp64 point of the metric)")
     ap.add_argument("--mode", default="global", choices=["global", "fixed", "fixed3"],
                     help="global: 3 kernels + allreduce (north star, default); fixed: R bounds (0, 2), "
                          "one fused kernel per step (N1); fixed3: R bounds (0, 2) on the stage kernels")
@@ -258,11 +268,15 @@ def main():
         group = dist.group.WORLD
 
     nq = args.nq
+    f64 = args.dtype == "f64"
+    if f64 and args.mode == "fixed":
+        raise SystemExit("--mode fixed (the fused kernel) is fp32 only; use fixed3 for fp64")
+    tdt = torch.float64 if f64 else torch.float32
     x, y, z = datagen.make_data({"nd": ND, "data": "uniform"}, seed=SEED)
     qx_np, qy_np = datagen.uniform_points(SEED, nq, datagen.S_QX, datagen.S_QY, offset=rank * nq)
-    eng = P.AIDW(x, y, z, dtype=torch.float32, device=gpu)
-    qx = torch.as_tensor(qx_np, dtype=torch.float32, device=dev)
-    qy = torch.as_tensor(qy_np, dtype=torch.float32, device=dev)
+    eng = P.AIDW(x, y, z, dtype=tdt, device=gpu)
+    qx = torch.as_tensor(qx_np, dtype=tdt, device=dev)
+    qy = torch.as_tensor(qy_np, dtype=tdt, device=dev)
     st = torch.cuda.current_stream(dev)
     flush = None if args.profile else torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
 
@@ -270,11 +284,11 @@ def main():
     if exchange:  # device-side bounds exchange over peer memory
         from paper_1511_02186_b200.partition import connect_exchange
         connect_exchange(eng, group)
-    r_obs = torch.empty(nq, dtype=torch.float32, device=dev)
+    r_obs = torch.empty(nq, dtype=tdt, device=dev)
     d1 = torch.empty_like(r_obs)
     al = torch.empty_like(r_obs)
     zo = torch.empty_like(r_obs)
-    mm = torch.empty(2, dtype=torch.float32, device=dev)
+    mm = torch.empty(2, dtype=tdt, device=dev)
     lv = datagen.ALPHA_LEVELS
 
     def step_fixed(ev=None):
@@ -338,9 +352,9 @@ def main():
     # ---- e2e: public API from pinned host buffers, H2D + D2H inside the timed region
     e2e = None
     if not args.no_e2e:
-        hx = torch.as_tensor(qx_np, dtype=torch.float32).pin_memory()
-        hy = torch.as_tensor(qy_np, dtype=torch.float32).pin_memory()
-        hz = torch.empty(nq, dtype=torch.float32).pin_memory()
+        hx = torch.as_tensor(qx_np, dtype=tdt).pin_memory()
+        hy = torch.as_tensor(qy_np, dtype=tdt).pin_memory()
+        hz = torch.empty(nq, dtype=tdt).pin_memory()
         e2e_steps = max(1, min(args.steps, 3))
         if group is not None:
             dist.barrier()
@@ -376,8 +390,9 @@ def main():
             t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
+        tb = 8 if f64 else 4
         e2e = {"value": nq * world / (e2e_ms / 1e3), "unit": "points/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": 2 * 4 * nq * world, "d2h_bytes_per_step": 4 * nq * world,
+               "h2d_bytes_per_step": 2 * tb * nq * world, "d2h_bytes_per_step": tb * nq * world,
                "api": ("aidw_run_fixed + torch H2D/D2H (pinned)" if args.mode == "fixed" else
                        "AIDW.run(FIXED) + torch H2D/D2H (pinned)" if args.mode == "fixed3" else
                        "aidw_run_host (C ABI, pinned host buffers)" if group is None and not exchange else
@@ -398,7 +413,8 @@ def main():
     interp_ms = float(per[:, 3].mean())
     # dominant kernel: the weighting pass, bound by the SFU + FMA pipes together
     interp_rate = pairs / (interp_ms / 1e3)
-    fr = class_fractions(al, d1) if args.mode != "fixed" else {"general": 1.0, "a1": 0.0, "a2": 0.0, "a3": 0.0}
+    fr = (class_fractions(al, d1) if args.mode != "fixed" and not f64 else
+          {"general": 1.0, "a1": 0.0, "a2": 0.0, "a3": 0.0})
     w_clk = weight_clk_mix(fr)
     sfu_peak_pairs = N_SM * f_max / w_clk
     path_clk_per_pair = KNN_FP32_PER_PAIR / FMA_PER_CLK_SM + w_clk
@@ -418,6 +434,16 @@ def main():
                 "peak_basis": "kNN 4 FP32/pair on the FMA pipe + the pipe-balanced weighting bound "
                               f"({w_clk:.4f} clk/pair), {N_SM} SM x {f_max / 1e6:.0f} MHz"}
         phases = {"fused": knn_ms}
+    elif f64:  # the fp64 weighting pass: FP64-pipe bound
+        dp_peak_pairs = N_SM * f_max * DFMA_PER_CLK_SM / DP_PER_PAIR
+        roof = {"bound": "alu", "kernel": "interp_kernel<double> (S5 weighting pass, fp64)",
+                "achieved": interp_rate / 1e9, "peak": dp_peak_pairs / 1e9, "unit": "Gpair/s",
+                "frac": interp_rate / dp_peak_pairs, "traffic": None,
+                "peak_basis": f"{N_SM} SM x {f_max / 1e6:.0f} MHz x {DFMA_PER_CLK_SM} FP64 instr/clk/SM "
+                              f"(tools/pipe_peaks.cu) / {DP_PER_PAIR} FP64 instructions per pair (SASS count)",
+                "frac_at_measured_clock": (interp_rate / dp_peak_pairs) * (f_max / (clocks["sm_mhz"] * 1e6))
+                if clocks.get("sm_mhz") else None}
+        phases = {"knn_robs": knn_ms, "allreduce": ar_ms, "alpha": alpha_ms, "interpolate": interp_ms}
     else:
         roof = None
         phases = {"knn_robs": knn_ms, "allreduce": ar_ms, "alpha": alpha_ms, "interpolate": interp_ms}
@@ -426,7 +452,7 @@ def main():
         rate, cores, sample = cpu_oracle_rate(x, y, z, qx_np, qy_np)
         cpu = {"value": rate, "unit": "points/s", "cores": cores, "kind": "oracle", "sample": sample}
     out = {
-        "metric": METRIC,
+        "metric": METRIC.replace("(fp32;", "(fp64;") if f64 else METRIC,
         "value": value,
         "unit": "points/s",
         "n_gpus": world,
@@ -436,9 +462,9 @@ def main():
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32",
+        "dtype": args.dtype,
         "data": "synthetic",
-        "config": {"workload": workload_name(world, nq, args.mode), "nd": ND, "nq_per_gpu": nq, "nq_total": nq * world,
+        "config": {"workload": workload_name(world, nq, args.mode, args.dtype), "nd": ND, "nq_per_gpu": nq, "nq_total": nq * world,
                    "k": K_NN, "alpha_levels": list(lv),
                    "rbounds": {"global": "global", "fixed": "fixed (0, 2), fused single kernel",
                                "fixed3": "fixed (0, 2), stage kernels"}[args.mode],

@@ -68,6 +68,42 @@ __global__ void bench(float *out, Clk *clk, float seed)
     if (blockIdx.x == 0 && threadIdx.x == 0) *clk = Clk{c0, c1, t0, t1};
 }
 
+// FP64 DFMA throughput (the fp64 weighting pass's pipe)
+__global__ void bench_dfma(float *out, Clk *clk, float seed)
+{
+    double v[kChains];
+#pragma unroll
+    for (int i = 0; i < kChains; ++i) v[i] = seed + threadIdx.x * 1e-7 + i * 1e-3;
+    unsigned long long c0 = clock64(), t0 = gtime();
+    for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+        for (int i = 0; i < kChains; ++i) v[i] = fma(v[i], 1.0000001, 1e-7);
+    }
+    unsigned long long c1 = clock64(), t1 = gtime();
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < kChains; ++i) s += v[i];
+    if (s == 12345.0) out[0] = (float)s;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *clk = Clk{c0, c1, t0, t1};
+}
+
+static double run_dfma(int sms, float *out, Clk *clk, double *mhz)
+{
+    const int threads = 1024, blocks = sms * 2;
+    bench_dfma<<<blocks, threads>>>(out, clk, 0.5f);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaEventRecord(a);
+    bench_dfma<<<blocks, threads>>>(out, clk, 0.5f);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    Clk h; cudaMemcpy(&h, clk, sizeof h, cudaMemcpyDeviceToHost);
+    *mhz = (double)(h.c1 - h.c0) / (double)(h.t1 - h.t0) * 1e3;
+    const double ops = (double)blocks * threads * kIters * kChains;
+    return ops / (ms * 1e-3) / (*mhz * 1e6) / sms;
+}
+
 template <int MODE> static double run(int sms, float *out, Clk *clk, double *mhz)
 {
     const int threads = 1024, blocks = sms * 2;
@@ -100,6 +136,9 @@ int main()
     double b7 = run<7>(sms, out, clk, &m7), b8 = run<8>(sms, out, clk, &m8);
     // mode 7: values updated = 2 FMAs per FFMA2; mode 8: 2 FFMA2 (4 FMAs) per 4 values
     printf("{\"ffma2_bcast_fma_per_clk_sm\": %.2f, \"ffma2_filter_pair_fma_per_clk_sm\": %.2f}\n", b7, b8);
+    double m9;
+    const double df = run_dfma(sms, out, clk, &m9);
+    printf("{\"dfma_per_clk_sm\": %.2f, \"sm_mhz\": %.0f}\n", df, m9);
     // modes 3/4 count values updated: mode 3 = FMAs (2 per FFMA2 instruction), mode 4 = 1 ex2 + 7 FFMA
     printf("{\"sms\": %d, \"mufu_ex2_per_clk_sm\": %.2f, \"mufu_lg2_per_clk_sm\": %.2f, \"ffma_per_clk_sm\": %.2f, "
            "\"ffma2_fma_per_clk_sm\": %.2f, \"ffma2_instr_per_clk_sm\": %.2f, \"mix_1ex2_7ffma_ops_per_clk_sm\": %.2f, "
