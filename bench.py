@@ -54,7 +54,7 @@ N_SM = 148
 # profiles/r01_ncu_interp_f64_v12.json) on the FP64 pipe; DFMA rate measured by
 # tools/pipe_peaks.cu (profiles/r01_pipe_peaks.json).
 DP_PER_PAIR = 25
-DFMA_PER_CLK_SM = 64.0
+DFMA_PER_CLK_SM = 63.23  # measured (profiles/r01_pipe_peaks.json dfma_per_clk_sm)
 
 
 def weight_clk_per_pair(fp32=WEIGHT_FP32_PER_PAIR, transc=TRANSC_PER_PAIR):
