@@ -138,6 +138,32 @@ def test_C4_full_size_sampled(P, orc):
     assert rel_err(z_g[sub], Zo).max() <= 1e-4
 
 
+def test_C4_full_size_sampled_f64(P, orc):
+    """1M x 1M in fp64 (the launch configuration of `bench.py --dtype f64`: spatial
+    order, seeded split, fp32 filter with fp64 re-check, fp64 weighting): r_obs and d1
+    bit-exact against the fp64 oracle on a strided sample, the GLOBAL bounds the exact
+    min/max of r_obs, sampled alpha and Z within 1e-10 of the oracle chain."""
+    x, y, z = datagen.make_data("C4")
+    qx, qy = datagen.make_queries("C4")
+    eng = P.AIDW(x, y, z, dtype=torch.float64)
+    Q = lambda v: torch.as_tensor(v, dtype=torch.float64, device="cuda")
+    tqx, tqy = Q(qx), Q(qy)
+    r, d1, mm = eng.knn_robs(tqx, tqy, 10)
+    sub = np.concatenate([np.arange(0, len(qx), 7993), [len(qx) - 1]])  # 130 queries
+    ro, do = orc.knn_f64(x, y, qx[sub], qy[sub], 10, want_dists=True)
+    assert np.array_equal(r.cpu().numpy()[sub], ro)
+    assert np.array_equal(np.sqrt(d1.cpu().numpy()[sub]), do[:, 0])
+    rc, mmc = r.cpu().numpy(), mm.cpu().numpy()
+    assert mmc[0] == -rc.min() and mmc[1] == rc.max()
+    a_g = eng.alpha(r, LV, P.GLOBAL, 0, 0, mm)
+    z_g = eng.interpolate(tqx, tqy, a_g, d1).cpu().numpy()
+    re = eng.r_exp
+    a_o = orc.alpha(ro, re, LV, -float(mmc[0]) / re, float(mmc[1]) / re)
+    assert np.max(np.abs(a_g.cpu().numpy()[sub] - a_o)) < 1e-14
+    Zo = orc.idw(x, y, z, qx[sub], qy[sub], a_o)
+    assert rel_err(z_g[sub], Zo).max() <= 1e-10
+
+
 # ------------------------------------------------------------------ edge cases
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 @pytest.mark.parametrize("nd,nq,k", [(5, 7, 5), (1, 3, 1), (1500, 1, 3), (3001, 777, 32), (2049, 300, 1),
