@@ -146,6 +146,7 @@ def cpu_oracle_rate(x, y, z, qx, qy, target_s=12.0):
     """Time the oracle as it stands (all host cores) on a bounded query sample of the
     workload; returns (points/s, cores, sample description)."""
     import oracle
+    oracle.set_num_threads(len(os.sched_getaffinity(0)))
     cores = oracle.num_threads()
     # calibrate with a small sample, then size the sample for ~target_s seconds
     n0 = max(cores, 16)
@@ -183,6 +184,8 @@ def run_reference(args):
     qx, qy = datagen.uniform_points(SEED, NQ_PER_GPU * args.gpus, datagen.S_QX, datagen.S_QY)
     import oracle
     oracle.build()
+    # rank 0 runs alone: use every host core it may run on (torchrun sets OMP_NUM_THREADS=1)
+    oracle.set_num_threads(len(os.sched_getaffinity(0)))
     cores = oracle.num_threads()
     # each step: a bounded sample sized so the whole run ends within minutes
     per_step = max(cores, int(args.ref_queries_per_step or 32 * cores))
