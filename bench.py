@@ -212,13 +212,26 @@ def run_reference(args):
     return 0
 
 
-def workload_name(n, nq=NQ_PER_GPU, mode="global", dtype="f32"):
+def query_block(rank, world, nq, strong):
+    """This rank's queries as (first index, count, job total): weak scaling gives every rank
+    ``nq`` queries; strong scaling splits ``nq`` into contiguous blocks [r nq/N, (r+1) nq/N)
+    (SURVEY §8(e)), so the ranks' blocks concatenate to the 1-GPU batch."""
+    if strong:
+        q0 = rank * nq // world
+        return q0, (rank + 1) * nq // world - q0, nq
+    return rank * nq, nq, nq * world
+
+
+def workload_name(n, nq=NQ_PER_GPU, mode="global", dtype="f32", nq_total=None):
     rb = {"global": "GLOBAL R bounds", "fixed": "FIXED R bounds (0, 2), fused kernel",
           "fixed3": "FIXED R bounds (0, 2), stage kernels"}[mode]
     prec = "fp64" if dtype == "f64" else "fp32"
     if n == 1:
         tag = ("C4" if nq == NQ_PER_GPU else "C4-shaped") + (" (fp64)" if dtype == "f64" else "")
         return f"{tag}: 1,024,000 data x {nq:,} queries, k=10, {prec}, uniform, {rb}"
+    if nq_total is not None:  # strong scaling: a fixed total split over n GPUs
+        return (f"C4 strong-scaled: 1,024,000 data x {nq_total:,} queries over {n} GPUs (~{nq} per GPU), "
+                f"k=10, {prec}, uniform, {rb}" + (f" allreduced over {n} GPUs" if mode == "global" else ""))
     return (f"C4 weak-scaled: 1,024,000 data x {n}x{nq:,} queries ({nq} per GPU), k=10, {prec}, "
             f"uniform, {rb}" + (f" allreduced over {n} GPUs" if mode == "global" else ""))
 
@@ -232,7 +245,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no baselines, no flush)")
-    ap.add_argument("--nq", type=int, default=NQ_PER_GPU, help="queries per GPU (default C4)")
+    ap.add_argument("--nq", type=int, default=NQ_PER_GPU,
+                    help="queries per GPU (weak scaling, default C4) or in total (--scaling strong)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: --nq queries per GPU (default); strong: --nq queries in total, "
+                         "rank r takes the contiguous block [r nq/N, (r+1) nq/N) (BASELINE C4: 1 vs 8 GPUs)")
     ap.add_argument("--ref-queries-per-step", type=int, default=0)
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
                     help="GLOBAL bounds: NCCL allreduce(MAX) (default) or the device-side push over "
@@ -270,13 +287,14 @@ def main():
             dist.init_process_group(backend)
         group = dist.group.WORLD
 
-    nq = args.nq
+    strong = args.scaling == "strong"
+    q0, nq, nq_total = query_block(rank, world, args.nq, strong)
     f64 = args.dtype == "f64"
     if f64 and args.mode == "fixed":
         raise SystemExit("--mode fixed (the fused kernel) is fp32 only; use fixed3 for fp64")
     tdt = torch.float64 if f64 else torch.float32
     x, y, z = datagen.make_data({"nd": ND, "data": "uniform"}, seed=SEED)
-    qx_np, qy_np = datagen.uniform_points(SEED, nq, datagen.S_QX, datagen.S_QY, offset=rank * nq)
+    qx_np, qy_np = datagen.uniform_points(SEED, nq, datagen.S_QX, datagen.S_QY, offset=q0)
     eng = P.AIDW(x, y, z, dtype=tdt, device=gpu)
     qx = torch.as_tensor(qx_np, dtype=tdt, device=dev)
     qy = torch.as_tensor(qy_np, dtype=tdt, device=dev)
@@ -394,8 +412,8 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         tb = 8 if f64 else 4
-        e2e = {"value": nq * world / (e2e_ms / 1e3), "unit": "points/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": 2 * tb * nq * world, "d2h_bytes_per_step": tb * nq * world,
+        e2e = {"value": nq_total / (e2e_ms / 1e3), "unit": "points/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 2 * tb * nq_total, "d2h_bytes_per_step": tb * nq_total,
                "api": ("aidw_run_fixed + torch H2D/D2H (pinned)" if args.mode == "fixed" else
                        "AIDW.run(FIXED) + torch H2D/D2H (pinned)" if args.mode == "fixed3" else
                        "aidw_run_host (C ABI, pinned host buffers)" if group is None and not exchange else
@@ -428,7 +446,7 @@ def main():
         traffic = tr.get("interp_dram_bytes_per_launch")
     except Exception:
         pass
-    value = nq * world / (ms / 1e3)
+    value = nq_total / (ms / 1e3)
     if args.mode == "fixed":  # one fused kernel per step: its roofline is the path bound
         fused_rate = pairs / (knn_ms / 1e3)
         roof = {"bound": "alu", "kernel": "fused_fixed_kernel (N1: S1..S5 in one launch)",
@@ -463,11 +481,12 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": args.dtype,
         "data": "synthetic",
-        "config": {"workload": workload_name(world, nq, args.mode, args.dtype), "nd": ND, "nq_per_gpu": nq, "nq_total": nq * world,
+        "config": {"workload": workload_name(world, nq, args.mode, args.dtype, nq_total if strong else None),
+                   "nd": ND, "nq_per_gpu": nq, "nq_total": nq_total,
                    "k": K_NN, "alpha_levels": list(lv),
                    "rbounds": {"global": "global", "fixed": "fixed (0, 2), fused single kernel",
                                "fixed3": "fixed (0, 2), stage kernels"}[args.mode],
@@ -476,8 +495,8 @@ def main():
                    "parallelism": f"query-sharded x{world}, data replicated",
                    "bounds_exchange": ("device push over peer memory (aidw_exchange_*)" if exchange else
                                        "NCCL allreduce(MAX)" if world > 1 else "local")},
-        "pair_evals_per_s": 2 * pairs * world / (ms / 1e3),
-        "aidw_pairs_per_s": pairs * world / (ms / 1e3),
+        "pair_evals_per_s": 2.0 * nq_total * ND / (ms / 1e3),
+        "aidw_pairs_per_s": float(nq_total) * ND / (ms / 1e3),
         "phases_ms": phases,
         "roofline": roof or {
             "bound": "alu", "kernel": "interp_kernel (S5 weighting pass)",

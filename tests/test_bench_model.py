@@ -41,3 +41,19 @@ def test_class_fractions_and_mix():
     assert mix < bench.weight_clk_per_pair()  # exact-exponent classes only lower the bound
     assert math.isclose(bench.weight_clk_mix({"general": 1.0, "a1": 0, "a2": 0, "a3": 0}),
                         bench.weight_clk_per_pair())
+
+
+@pytest.mark.parametrize("nq,world", [(1_024_000, 8), (1_024_000, 3), (7, 4), (0, 2), (5, 1)])
+def test_query_blocks_strong(nq, world):
+    # strong scaling: contiguous blocks that tile [0, nq) exactly, sizes differ by <= 1
+    blocks = [bench.query_block(r, world, nq, True) for r in range(world)]
+    assert all(t == nq for _, _, t in blocks)
+    assert blocks[0][0] == 0
+    for (a0, an, _), (b0, _, _) in zip(blocks, blocks[1:]):
+        assert a0 + an == b0
+    assert blocks[-1][0] + blocks[-1][1] == nq
+    assert max(n for _, n, _ in blocks) - min(n for _, n, _ in blocks) <= 1
+
+
+def test_query_blocks_weak():
+    assert [bench.query_block(r, 4, 100, False) for r in range(4)] == [(r * 100, 100, 400) for r in range(4)]
