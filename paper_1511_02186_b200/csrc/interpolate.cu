@@ -429,6 +429,19 @@ static int interp_variant()
     return v;
 }
 
+// True when the Q = 2 grid, split into every accumulation block, stays under one wave of
+// 8 CTAs per SM (AIDW_INTERP_Q1=0 disables, =1 forces; tests).
+static bool small_grid(int64_t nq, int64_t ndp)
+{
+    const char *e = getenv("AIDW_INTERP_Q1");
+    if (e) return e[0] == '1';
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ctas = (nq + 2 * kBlock - 1) / (2 * kBlock) * acc_blocks((int)(ndp / kTileW));
+    return ctas < (int64_t)sms * 8;
+}
+
 static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st, SplitBuf *sp)
 {
     // EMU: 2-bit mode per couple h of 4-point group g at bit 4g+2h (passes.cuh)
@@ -468,8 +481,13 @@ static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st, SplitB
     case 33: return launch_interp_f32x2<2, 0x4105>(a, st, sp);  // Q = 2, f = 4/8 (0, 1, 4, 7)
     case 34: return launch_interp_f32x2<2, 0x0141>(a, st, sp);  // Q = 2, f = 3/8
     case 35: return launch_interp_f32x2<1, 0x0141>(a, st, sp);  // Q = 1, f = 3/8 (default before v10)
-    default: return launch_interp_f32x2<2, 0x4141>(a, st, sp);  // Q = 2, f = 4/8 spread (best measured, r01 v10)
+    default: break;
     }
+    // Q = 2, f = 4/8 spread (best measured, r01 v10); a grid that does not fill one wave
+    // even when fully split (small nq: C1, C2, a serving batch) takes Q = 1 for twice the
+    // CTAs -- same per-point offload pattern, so Z is bit-identical (test_interp_q1_small_grid)
+    if (small_grid(a.nq, a.ndp)) return launch_interp_f32x2<1, 0x4141>(a, st, sp);
+    return launch_interp_f32x2<2, 0x4141>(a, st, sp);
 }
 
 // N4: Z from P shards' partials [P][nq][4], summed in rank order (deterministic).
@@ -527,6 +545,7 @@ int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const vo
     InterpArgs<double> a{p, p + ndp, p + 2 * ndp, ndp, nd, (const double *)qx, (const double *)qy,
                          (const double *)alpha, (const double *)d1sq, nq, (double *)z, alpha_const, partial,
                          nullptr, nullptr};
+    if (small_grid(nq, ndp)) return launch_interp_t<double, 1>(a, st, split);
     return launch_interp_t<double, 2>(a, st, split);
 }
 

@@ -459,9 +459,13 @@ template <typename T, int K, int Q, int G, bool SPLIT, int MINB> static int set_
 // AIDW_KNN_ORDER=0 disables (tests compare both).
 static bool order_queries(int64_t nq)
 {
-    constexpr int64_t kOrderMinQ = 32768;
+    static int64_t min_q = -1;
+    if (min_q < 0) {  // AIDW_KNN_ORDER_MIN: tuning knob for the threshold (tools/tune_knn.py)
+        const char *m = getenv("AIDW_KNN_ORDER_MIN");
+        min_q = m ? atoll(m) : 32768;
+    }
     const char *e = getenv("AIDW_KNN_ORDER");
-    return nq >= kOrderMinQ && nq <= INT_MAX && !(e && e[0] == '0');  // perm is int32
+    return nq >= min_q && nq > 0 && nq <= INT_MAX && !(e && e[0] == '0');  // perm is int32
 }
 
 template <int K, int Q, int G = 8, int MINB = 0, typename T = float>
@@ -567,7 +571,7 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
     if (k <= 4) return launch_knn_filter_t<4, 2, 16>(a, f, st, sp, fd);
     if (k <= 8) return launch_knn_filter_t<8, 2, 16>(a, f, st, sp, fd);
     if (k <= 10) {  // large (spatially ordered) batches: Q = 4, G = 32 (108 vs 115 ms at C4)
-        if (order_queries(a.nq)) return launch_knn_filter_t<10, 4, 32>(a, f, st, sp, fd);
+        if (order_queries(a.nq) && a.nq >= 32768) return launch_knn_filter_t<10, 4, 32>(a, f, st, sp, fd);
         return launch_knn_filter_t<10, 2, 16>(a, f, st, sp, fd);
     }
     if (k <= 12) return launch_knn_filter_t<12, 2, 16>(a, f, st, sp, fd);

@@ -323,6 +323,38 @@ def test_split_bit_identical(P, monkeypatch, dtype, nd, nq, k):
             assert np.array_equal(u, v, equal_nan=True), (sv, n)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("nd,nq", [(1024, 1024), (10240, 3000), (5000, 777)])
+def test_interp_q1_small_grid(P, orc, monkeypatch, dtype, nd, nq):
+    """Small grids run the weighting pass with Q = 1 query per thread instead of 2
+    (DESIGN.md §4.3): the exp2 offload pattern depends only on the data-point index, so Z
+    (run, idw, classes, coincident queries) is bit-identical for Q = 1 and Q = 2, split or
+    not, and within tolerance of the oracle."""
+    x, y, z, qx, qy = datagen.random_cloud(900 + nq, nd, nq)
+    qx[::11], qy[::11] = x[: len(qx[::11])], y[: len(qy[::11])]
+    eng = P.AIDW(x, y, z, dtype=dtype)
+    outs = {}
+    for q1 in ("0", "1"):
+        monkeypatch.setenv("AIDW_INTERP_Q1", q1)
+        for sv in ("0", None):
+            if sv is None:
+                monkeypatch.delenv("AIDW_SPLIT", raising=False)
+            else:
+                monkeypatch.setenv("AIDW_SPLIT", sv)
+            zr = eng.run(qx, qy, 10, LV, P.GLOBAL)
+            zi = eng.idw(qx, qy, 2.0)
+            outs[(q1, sv)] = [t.cpu().numpy() for t in (zr, zi)]
+    monkeypatch.delenv("AIDW_INTERP_Q1")
+    monkeypatch.delenv("AIDW_SPLIT", raising=False)
+    ref = outs[("0", "0")]
+    for key, o in outs.items():
+        for n, (u, v) in enumerate(zip(o, ref)):
+            assert np.array_equal(u, v), (key, n)
+    assert rel_err(ref[0], orc.aidw(x, y, z, qx, qy, 10, LV, mode="global")).max() <= TOL[dtype]
+    eng.close()
+
+
 @pytest.mark.parametrize("case", ["C3", "outside", "duplicates"])
 def test_knn_order_bit_identical(P, orc, monkeypatch, case):
     """Spatial order (Morton-sorted data copy, query permutation, per-CTA

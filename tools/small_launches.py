@@ -1,5 +1,5 @@
 """Run the whole GLOBAL path once per small config (C1, C2 f32/f64, C3) after a warm-up,
-for an ncu launch list (`--metrics gpu__time_duration.sum`): which kernels the small
+for an ncu launch list (`--metrics gpu__time_duration.sum --profile-from-start off`): which kernels the small
 configs spend their time in.  usage: ncu ... python tools/small_launches.py"""
 import os
 import sys
@@ -21,9 +21,9 @@ for name, dt in (("C1", torch.float64), ("C2", torch.float32), ("C2", torch.floa
     for _ in range(2):
         eng.run(tqx, tqy, k=k)
     torch.cuda.synchronize()
-    torch.cuda.nvtx.range_push(f"{name}_{dt}")
+    torch.cuda.profiler.start()  # ncu --profile-from-start off: only this run is listed
     eng.run(tqx, tqy, k=k)
     torch.cuda.synchronize()
-    torch.cuda.nvtx.range_pop()
+    torch.cuda.profiler.stop()
     print(name, dt, flush=True)
     eng.close()
