@@ -606,14 +606,27 @@ __global__ void __launch_bounds__(kBlock) knn_merge_kernel(const KnnArgs<T> a, c
     const int k0 = K - a.k;
 #pragma unroll
     for (int i = 0; i < K; ++i) buf[0][i] = (i < k0) ? -pos_inf<T>() : pos_inf<T>();
-    if (valid[0])
+    if (valid[0]) {
+        // a list's k values are loaded together (and the next list's while this one is
+        // inserted), so the merge costs about one L2 latency per list, not per value;
+        // the insertion sequence -- hence the merged multiset -- is unchanged
+        T v[K], nx[K];
+        const T *l = lists + base * a.k;
+#pragma unroll
+        for (int i = 0; i < K; ++i) nx[i] = i < a.k ? __ldg(l + i) : pos_inf<T>();
         for (int p = 0; p < P; ++p) {
-            const T *l = lists + ((int64_t)p * a.nq + base) * a.k;
-            for (int i = 0; i < a.k; ++i) {
-                const T s = l[i];
-                if (s < buf[0][K - 1]) topk_insert<T, K>(buf[0], s);
+#pragma unroll
+            for (int i = 0; i < K; ++i) v[i] = nx[i];
+            if (p + 1 < P) {
+                const T *ln = lists + ((int64_t)(p + 1) * a.nq + base) * a.k;
+#pragma unroll
+                for (int i = 0; i < K; ++i) nx[i] = i < a.k ? __ldg(ln + i) : pos_inf<T>();
             }
+#pragma unroll
+            for (int i = 0; i < K; ++i)
+                if (i < a.k && v[i] < buf[0][K - 1]) topk_insert<T, K>(buf[0], v[i]);
         }
+    }
     const int64_t qid[Q] = {base};
     knn_epilogue<T, K, Q>(a, buf, valid, qid, k0);
 }
