@@ -295,7 +295,9 @@ __global__ void __launch_bounds__(kBlock) knn_robs_kernel(const KnnArgs<T> a)
 // registers and was measured slower: 113 vs 108 ms at C4).
 template <typename T> __host__ __device__ constexpr int filter_arrays() { return sizeof(T) == 4 ? 5 : 3; }
 
-template <typename T, int K, int Q, int G, bool SPLIT, int MINB = 0>
+// SPLIT: 0 = whole data range; 1 = a split (seeded from the home tile when the batch is
+// spatially ordered); 2 = an unordered split with the per-query seed (seed_query).
+template <typename T, int K, int Q, int G, int SPLIT, int MINB = 0>
 __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<T> a, const FilterArgs f)
 {
     constexpr int TILE = kTileKF, STAGES = kStagesKF, NARR = filter_arrays<T>();
@@ -362,6 +364,13 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
     KnnF32State<K, Q, T> st;
 #pragma unroll
     for (int q = 0; q < Q; ++q) st.init(q, qx[q], qy[q], f, k0);
+    if constexpr (SPLIT == 2) {  // unordered split: per-query seed (null pointers: off)
+        if (!seed && (f.sx64 != nullptr || f.sx != nullptr)) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (valid[q]) st.seed_query(q, f, a.k, k0);
+        }
+    }
 
     for (int t = 0; t < ntiles; ++t) {
         ring.wait_full(t);
@@ -446,7 +455,7 @@ template <typename T> static int knn_finish(const KnnArgs<T> &a, int S, cudaStre
 }
 
 // ---------------------------------------------------------------------------------
-template <typename T, int K, int Q, int G, bool SPLIT, int MINB> static int set_filter_attrs(size_t smem)
+template <typename T, int K, int Q, int G, int SPLIT, int MINB> static int set_filter_attrs(size_t smem)
 {
     auto kern = knn_filter_kernel<T, K, Q, G, SPLIT, MINB>;
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
@@ -468,23 +477,31 @@ static bool order_queries(int64_t nq)
     return nq >= min_q && nq > 0 && nq <= INT_MAX && !(e && e[0] == '0');  // perm is int32
 }
 
+// Unordered split launches seed each query's lists from the sorted copy (§4.6);
+// AIDW_KNN_SEED=0 disables (tests compare both).
+static bool seed_unordered()
+{
+    const char *e = getenv("AIDW_KNN_SEED");
+    return !(e && e[0] == '0');
+}
+
 template <int K, int Q, int G = 8, int MINB = 0, typename T = float>
 static int launch_knn_filter_t(KnnArgs<T> a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp,
                                FilterData *fd)
 {
     const size_t smem =
         (size_t)filter_arrays<T>() * kStagesKF * kTileKF * sizeof(float) + 2 * kStagesKF * sizeof(uint64_t);
-    if (set_filter_attrs<T, K, Q, G, false, MINB>(smem) < 0) return -1;
+    if (set_filter_attrs<T, K, Q, G, 0, MINB>(smem) < 0) return -1;
     const int64_t per_cta = (int64_t)kBlock * Q;
     const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
     // A spatially ordered batch splits only with seeded lists (knn_filter_kernel), by the
     // factor that best fills the last wave (ordered_split_factor); an unordered one by
     // whole extra waves (knn_split_factor: its splits restart the top-k warm-up).
     const bool ordered = fd && fd->cell_start && order_queries(a.nq);
-    if (ordered && set_filter_attrs<T, K, Q, G, true, MINB>(smem) < 0) return -1;
-    const int S = ordered ? ordered_split_factor((const void *)knn_filter_kernel<T, K, Q, G, true, MINB>, smem,
+    if (ordered && set_filter_attrs<T, K, Q, G, 1, MINB>(smem) < 0) return -1;
+    const int S = ordered ? ordered_split_factor((const void *)knn_filter_kernel<T, K, Q, G, 1, MINB>, smem,
                                                  grid, (int)(a.ndp / kTileKF), a, sp)
-                          : knn_split_factor((const void *)knn_filter_kernel<T, K, Q, G, false, MINB>, smem, grid,
+                          : knn_split_factor((const void *)knn_filter_kernel<T, K, Q, G, 0, MINB>, smem, grid,
                                              (int)(a.ndp / kTileKF), a, sp);
     int pre = 0;
     FilterArgs fo = f;
@@ -505,10 +522,25 @@ static int launch_knn_filter_t(KnnArgs<T> a, const FilterArgs &f, cudaStream_t s
         }
     }
     if (S == 1) {
-        knn_filter_kernel<T, K, Q, G, false, MINB><<<grid, kBlock, smem, st>>>(a, fo);
+        knn_filter_kernel<T, K, Q, G, 0, MINB><<<grid, kBlock, smem, st>>>(a, fo);
     } else {
-        if (set_filter_attrs<T, K, Q, G, true, MINB>(smem) < 0) return -1;
-        knn_filter_kernel<T, K, Q, G, true, MINB><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, fo);
+        if (!ordered && fd && fd->cell_start && seed_unordered()) {  // per-query seed (§4.6)
+            const float *c = static_cast<const float *>(fd->arrays);
+            if (fd->coords64) {
+                fo.sx64 = fd->coords64;
+                fo.sy64 = fd->coords64 + a.ndp;
+            } else {
+                fo.sx = c + 6 * a.ndp;
+                fo.sy = c + 7 * a.ndp;
+            }
+        }
+        if (ordered) {
+            if (set_filter_attrs<T, K, Q, G, 1, MINB>(smem) < 0) return -1;
+            knn_filter_kernel<T, K, Q, G, 1, MINB><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, fo);
+        } else {
+            if (set_filter_attrs<T, K, Q, G, 2, MINB>(smem) < 0) return -1;
+            knn_filter_kernel<T, K, Q, G, 2, MINB><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, fo);
+        }
     }
     const int n = knn_finish(a, S, st);
     return n < 0 ? -1 : n + pre;

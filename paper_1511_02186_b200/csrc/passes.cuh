@@ -95,6 +95,10 @@ struct FilterArgs {
     float r1;                   // R1 bound
     const int *cell_start;      // first sorted position of each Morton cell (§4.7)
     OrderGrid grid;
+    // unordered split launches: the Morton-sorted coordinates for the per-query seed
+    // (KnnF32State::seed_query); null = no seed
+    const float *sx = nullptr, *sy = nullptr;
+    const double *sx64 = nullptr, *sy64 = nullptr;
 };
 
 // thr_of: the filter threshold for the canonical k-th distance thr, in fp32 with every
@@ -160,6 +164,35 @@ struct KnnF32State {
             for (int i = 0; i < K; ++i) buf[q][i] = (i < k0) ? -pos_inf<T>() : v;
             thr[q] = thr_of(thr_f32(v), qqf[q], mf[q], Ef[q]);
         }
+    }
+    // Per-query seed for unordered split launches: the k real points at
+    // and after the query's Morton cell in the sorted copy (cell_start[kCells] = nd);
+    // their largest canonical s, v, bounds the query's k-th distance from above, so the
+    // list starts as k copies of v -- the argument of seed_lists.  A non-finite v (NaN or
+    // far queries, nd < k) leaves the list unseeded.
+    __device__ __forceinline__ void seed_query(int q, const FilterArgs &f, int k, int k0)
+    {
+        const T *sx, *sy;
+        if constexpr (sizeof(T) == 4) {
+            sx = f.sx;
+            sy = f.sy;
+        } else {
+            sx = f.sx64;
+            sy = f.sy64;
+        }
+        const int nd = f.cell_start[kCells];
+        if (sx == nullptr || nd < k) return;
+        int j0 = f.cell_start[morton_cell((float)qx[q], (float)qy[q], f.grid)];
+        j0 = j0 > nd - k ? nd - k : j0;
+        T v = T(0);
+        for (int i = 0; i < k; ++i) {
+            const T s = dist_sq(qx[q], qy[q], sx[j0 + i], sy[j0 + i]);
+            v = (s > v || s != s) ? s : v;  // max, NaN-propagating
+        }
+        if (!(v < pos_inf<T>())) return;
+#pragma unroll
+        for (int i = 0; i < K; ++i) buf[q][i] = (i < k0) ? -pos_inf<T>() : v;
+        thr[q] = thr_of(thr_f32(v), qqf[q], mf[q], Ef[q]);
     }
 };
 

@@ -355,6 +355,41 @@ def test_interp_q1_small_grid(P, orc, monkeypatch, dtype, nd, nq):
     eng.close()
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("nd,nq,k", [(10240, 2000, 10), (3000, 500, 15), (5000, 300, 1), (2048, 64, 32)])
+def test_knn_seed_unordered_split(P, orc, monkeypatch, dtype, nd, nq, k):
+    """Unordered split launches seed each query's lists with the largest canonical s of k
+    Morton-neighbour points: distance lists, r_obs, d1sq, bounds and Z
+    are bit-identical with the seed off, for several split factors, with duplicate data
+    points, coincident and outside queries; lists equal the oracle's."""
+    x, y, z, qx, qy = datagen.random_cloud(1700 + nq, nd, nq)
+    x[1::5], y[1::5] = x[0:-1:5][: len(x[1::5])], y[0:-1:5][: len(y[1::5])]  # duplicates
+    qx[::9], qy[::9] = x[: len(qx[::9])], y[: len(qy[::9])]  # coincident queries
+    qx[1], qy[1] = 1.75, -0.5  # outside the data bbox (s still exact in fp64, R16)
+    eng = P.AIDW(x, y, z, dtype=dtype)
+    outs = {}
+    for seed in ("0", "1"):
+        monkeypatch.setenv("AIDW_KNN_SEED", seed)
+        for sv in ("2", "5", None):
+            if sv is None:
+                monkeypatch.delenv("AIDW_SPLIT", raising=False)
+            else:
+                monkeypatch.setenv("AIDW_SPLIT", sv)
+            r, d1, mm, dd = eng.knn_robs(qx, qy, k, want_dists=True)
+            zr = eng.run(qx, qy, k, LV, P.GLOBAL)
+            outs[(seed, sv)] = [t.cpu().numpy() for t in (r, d1, mm, dd, zr)]
+    monkeypatch.delenv("AIDW_KNN_SEED")
+    monkeypatch.delenv("AIDW_SPLIT", raising=False)
+    ref = outs[("0", "2")]
+    for key, o in outs.items():
+        for n, (u, v) in enumerate(zip(o, ref)):
+            assert np.array_equal(u, v), (key, n)
+    ro, do = oracle_knn(orc, x, y, qx, qy, k, dtype)
+    assert np.array_equal(ref[3], do) and np.array_equal(ref[0], ro)
+    eng.close()
+
+
 @pytest.mark.parametrize("case", ["C3", "outside", "duplicates"])
 def test_knn_order_bit_identical(P, orc, monkeypatch, case):
     """Spatial order (Morton-sorted data copy, query permutation, per-CTA
