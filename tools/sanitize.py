@@ -32,6 +32,12 @@ for dt in (torch.float32, torch.float64):
     for v in (0, 1):
         P.aidw_paper_baseline(v, t, len(x), torch.as_tensor(qx, dtype=dt, device="cuda"),
                               torch.as_tensor(qy, dtype=dt, device="cuda"), 10, LV, eng.area, 0, 2, zo)
+    # per-query seed at the sorted copy's end (nd close to k: j0 clamped to nd - k) and a
+    # query outside the data bbox; small-grid (Q = 1) weighting
+    small = P.AIDW(x[:40], y[:40], z[:40], dtype=dt)
+    small.knn_robs(np.append(qx, 3.5), np.append(qy, -2.0), 32, want_dists=True)
+    small.run(qx, qy, 32, LV, P.GLOBAL)
+    small.close()
     # large batch: spatial query order + Q = 4 kNN (fp32), unsplit launches
     _, _, _, bx, by = datagen.random_cloud(6, 10, 40000)
     eng.run(bx, by, 10, LV, P.GLOBAL)
