@@ -407,8 +407,9 @@ static int knn_split_factor(const void *kern, size_t smem, unsigned grid, int nt
     return a.lists ? S : 1;
 }
 
-// Seeded split of a spatially ordered batch: the factor S <= 8 minimising the waves per
-// split, ceil(grid S / slots) / S, with each split's extra seed tile counted
+// Seeded split of a spatially ordered batch: the factor S <= 8 (>= 128 tiles per split)
+// minimising the waves per split, ceil(grid S / slots) / S, with each split's extra seed
+// tile counted
 // (C4: 2,000 CTAs on 592 slots -> S = 5, 17 waves of 1/5 instead of 4 of 1).
 // AIDW_SPLIT=0 disables, AIDW_SPLIT=n forces n (tests).
 template <typename T>
@@ -432,7 +433,10 @@ static int ordered_split_factor(const void *kern, size_t smem, unsigned grid, in
         }
         const double slots = (double)occ * sms;
         double best = 0.0;
-        for (int s = 1; s <= 8 && ntiles / s >= 8; ++s) {
+        // each split keeps >= 128 tiles: shorter ranges lose more to the per-CTA fixed
+        // costs (ring fill, seed tile, list write, merge) than the fuller wave gains
+        // (C3, 200 tiles: unsplit 1.83 ms, S = 3 1.90, S = 7 1.96; C4, 2000 tiles: S = 5)
+        for (int s = 1; s <= 8 && ntiles / s >= 128; ++s) {
             const double waves = std::ceil((double)grid * s / slots);
             const double cost = waves / s * (1.0 + (double)s / ntiles);
             if (s == 1 || cost < best * 0.995) {
