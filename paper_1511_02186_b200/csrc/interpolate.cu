@@ -429,9 +429,12 @@ static int interp_variant()
     return v;
 }
 
-// True when the Q = 2 grid, split into every accumulation block, stays under one wave of
-// 8 CTAs per SM (AIDW_INTERP_Q1=0 disables, =1 forces; tests).
-static bool small_grid(int64_t nq, int64_t ndp)
+// True when the Q = 2 grid, split into every accumulation block, has fewer than
+// `per_sm` CTAs per SM (AIDW_INTERP_Q1=0 disables, =1 forces; tests).  fp32 (9 CTAs/SM
+// resident): Q = 1 wins below ~5 waves (profiles/small/r01_q1_sweep_*.log, nd = 1M:
+// 20,000 queries 11.1 -> 9.7 ms, 100,000 40.1 -> 39.2; 128,000 49.5 vs 50.3 with Q = 1);
+// fp64: under one wave (C1, C2).
+static bool small_grid(int64_t nq, int64_t ndp, int per_sm)
 {
     const char *e = getenv("AIDW_INTERP_Q1");
     if (e) return e[0] == '1';
@@ -439,7 +442,7 @@ static bool small_grid(int64_t nq, int64_t ndp)
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t ctas = (nq + 2 * kBlock - 1) / (2 * kBlock) * acc_blocks((int)(ndp / kTileW));
-    return ctas < (int64_t)sms * 8;
+    return ctas < (int64_t)sms * per_sm;
 }
 
 static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st, SplitBuf *sp)
@@ -483,10 +486,11 @@ static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st, SplitB
     case 35: return launch_interp_f32x2<1, 0x0141>(a, st, sp);  // Q = 1, f = 3/8 (default before v10)
     default: break;
     }
-    // Q = 2, f = 4/8 spread (best measured, r01 v10); a grid that does not fill one wave
-    // even when fully split (small nq: C1, C2, a serving batch) takes Q = 1 for twice the
-    // CTAs -- same per-point offload pattern, so Z is bit-identical (test_interp_q1_small_grid)
-    if (small_grid(a.nq, a.ndp)) return launch_interp_f32x2<1, 0x4141>(a, st, sp);
+    // Q = 2, f = 4/8 spread (best measured, r01 v10); a grid of fewer than ~5 waves even
+    // when fully split (small nq: C1-C3, a strong-scaled share, a serving batch) takes
+    // Q = 1 for twice the CTAs -- same per-point offload pattern, so Z is bit-identical
+    // (test_interp_q1_small_grid)
+    if (small_grid(a.nq, a.ndp, 45)) return launch_interp_f32x2<1, 0x4141>(a, st, sp);
     return launch_interp_f32x2<2, 0x4141>(a, st, sp);
 }
 
@@ -545,7 +549,7 @@ int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const vo
     InterpArgs<double> a{p, p + ndp, p + 2 * ndp, ndp, nd, (const double *)qx, (const double *)qy,
                          (const double *)alpha, (const double *)d1sq, nq, (double *)z, alpha_const, partial,
                          nullptr, nullptr};
-    if (small_grid(nq, ndp)) return launch_interp_t<double, 1>(a, st, split);
+    if (small_grid(nq, ndp, 8)) return launch_interp_t<double, 1>(a, st, split);
     return launch_interp_t<double, 2>(a, st, split);
 }
 

@@ -1,5 +1,5 @@
 """Time interp variants (AIDW_INTERP_VARIANT) on C4 and check accuracy on a sample.
-Run one variant per process: python tools/tune_interp.py VARIANT [nq]"""
+Run one variant per process (AIDW_INTERP_VARIANT=v): python tools/tune_interp.py [nq] [--check]"""
 import os
 import sys
 import time
@@ -28,7 +28,8 @@ for _ in range(3):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); P.aidw_interpolate(eng.h, qx_t, qy_t, a, d1, zo); e1.record(); e1.synchronize()
     ts.append(e0.elapsed_time(e1))
-out = {"variant": os.environ.get("AIDW_INTERP_VARIANT", "0"), "interp_ms": min(ts),
+out = {"variant": os.environ.get("AIDW_INTERP_VARIANT", "0"), "q1": os.environ.get("AIDW_INTERP_Q1", "auto"),
+       "nq": nq, "interp_ms": min(ts),
        "gpairs_per_s": nq * len(x) / (min(ts) / 1e3) / 1e9}
 if "--check" in sys.argv:
     import oracle
