@@ -50,9 +50,9 @@ def lib():
         I64 = ctypes.c_int64
         D = ctypes.c_double
         L.oracle_knn_insert.argtypes = [P, ctypes.c_int, D]
-        L.oracle_knn_f64.argtypes = [P, P, I64, P, P, I64, ctypes.c_int, P, P]
+        L.oracle_knn_f64.argtypes = [P, P, I64, P, P, I64, ctypes.c_int, P, P, P]
         L.oracle_knn_f64.restype = ctypes.c_int
-        L.oracle_knn_f32.argtypes = [P, P, I64, P, P, I64, ctypes.c_int, P, P]
+        L.oracle_knn_f32.argtypes = [P, P, I64, P, P, I64, ctypes.c_int, P, P, P]
         L.oracle_knn_f32.restype = ctypes.c_int
         L.oracle_bbox_area.argtypes = [P, P, I64]
         L.oracle_bbox_area.restype = D
@@ -97,28 +97,29 @@ def knn_insert(buf, dist):
     return b
 
 
-def knn_f64(x, y, qx, qy, k, want_dists=False):
-    """k nearest distances (ascending) and r_obs per query, fp64 (§3.1.2, Eq. 3)."""
-    x, y, qx, qy = _f64(x), _f64(y), _f64(qx), _f64(qy)
+def _knn(fn, cast, npdt, x, y, qx, qy, k, want_dists, want_d1sq):
+    x, y, qx, qy = cast(x), cast(y), cast(qx), cast(qy)
     nq = qx.shape[0]
-    robs = np.empty(nq, np.float64)
-    d = np.empty((nq, k), np.float64) if want_dists else None
-    rc = lib().oracle_knn_f64(_p(x), _p(y), x.shape[0], _p(qx), _p(qy), nq, int(k), _p(d), _p(robs))
+    robs = np.empty(nq, npdt)
+    d = np.empty((nq, k), npdt) if want_dists else None
+    d1 = np.empty(nq, npdt) if want_d1sq else None
+    rc = fn(_p(x), _p(y), x.shape[0], _p(qx), _p(qy), nq, int(k), _p(d), _p(robs), _p(d1))
     if rc != 0:
-        raise ValueError("oracle_knn_f64: k out of range or nd < k")
-    return (robs, d) if want_dists else robs
+        raise ValueError("oracle kNN: k out of range or nd < k")
+    out = (robs,) + ((d,) if want_dists else ()) + ((d1,) if want_d1sq else ())
+    return out if len(out) > 1 else robs
 
 
-def knn_f32(x, y, qx, qy, k, want_dists=False):
+def knn_f64(x, y, qx, qy, k, want_dists=False, want_d1sq=False):
+    """k nearest distances (ascending) and r_obs per query, fp64 (§3.1.2, Eq. 3);
+    optionally the nearest squared distance min_i s_i (R16/R20).
+    Returns robs, or (robs[, dists][, d1sq])."""
+    return _knn(lib().oracle_knn_f64, _f64, np.float64, x, y, qx, qy, k, want_dists, want_d1sq)
+
+
+def knn_f32(x, y, qx, qy, k, want_dists=False, want_d1sq=False):
     """The fp32 instantiation (REAL = float; R16)."""
-    x, y, qx, qy = _f32(x), _f32(y), _f32(qx), _f32(qy)
-    nq = qx.shape[0]
-    robs = np.empty(nq, np.float32)
-    d = np.empty((nq, k), np.float32) if want_dists else None
-    rc = lib().oracle_knn_f32(_p(x), _p(y), x.shape[0], _p(qx), _p(qy), nq, int(k), _p(d), _p(robs))
-    if rc != 0:
-        raise ValueError("oracle_knn_f32: k out of range or nd < k")
-    return (robs, d) if want_dists else robs
+    return _knn(lib().oracle_knn_f32, _f32, np.float32, x, y, qx, qy, k, want_dists, want_d1sq)
 
 
 def bbox_area(x, y) -> float:

@@ -80,12 +80,21 @@ static void sort_ascending_f(float *a, int k)
         }
 }
 
-/* Euclidean distance in the plane, Eq. 1's d(x, x_i). */
-static double dist2d(double qx, double qy, double px, double py)
+/* Squared Euclidean distance in the plane, Eq. 1's d(x, x_i)^2,
+ * in the canonical sequence of DESIGN.md reading R16 (the paper's
+ * REAL arithmetic, fixes no operation order):
+ *   dx = qx - px; dy = qy - py; s = fma(dx, dx, dy*dy)   (each op rounded to nearest). */
+static double dist2d_sq(double qx, double qy, double px, double py)
 {
     double dx = qx - px;
     double dy = qy - py;
-    return sqrt(dx * dx + dy * dy);
+    return fma(dx, dx, dy * dy);
+}
+
+/* Euclidean distance d = sqrt_RN(s) (R16). */
+static double dist2d(double qx, double qy, double px, double py)
+{
+    return sqrt(dist2d_sq(qx, qy, px, py));
 }
 
 #define KMAX 64
@@ -95,26 +104,39 @@ static double dist2d(double qx, double qy, double px, double py)
  *   §3.1.2 Steps 1-3 give the k nearest distances d_1..d_k,
  *   Eq. 3: r_obs = (1/k) * sum_i d_i, summed in ascending order.
  * dists_out (nullable): [nq*k] ascending distances per query.
+ * d1sq_out (nullable): [nq] squared distance to the nearest data point, min_i s_i
+ *   (R16's s; the weighting pass scales Eq. 1's weights by it, R20).
  * Returns 0, or -1 if k is out of range / nd < k.
  */
 int oracle_knn_f64(const double *x, const double *y, int64_t nd,
                    const double *qx, const double *qy, int64_t nq, int k,
-                   double *dists_out, double *robs_out)
+                   double *dists_out, double *robs_out, double *d1sq_out)
 {
     if (k < 1 || k > KMAX || nd < k)
         return -1;
 #pragma omp parallel for schedule(static)
     for (int64_t q = 0; q < nq; ++q) {
         double buf[KMAX];
-        for (int i = 0; i < k; ++i) /* Step 1 */
-            buf[i] = dist2d(qx[q], qy[q], x[i], y[i]);
-        sort_ascending(buf, k);      /* Step 2 */
-        for (int64_t i = k; i < nd; ++i) /* Step 3 */
-            oracle_knn_insert(buf, k, dist2d(qx[q], qy[q], x[i], y[i]));
+        double m = INFINITY;
+        for (int64_t i = 0; i < nd; ++i) {
+            double s = dist2d_sq(qx[q], qy[q], x[i], y[i]);
+            if (s < m)
+                m = s;
+            double d = sqrt(s);
+            if (i < k) { /* Step 1: the first k distances */
+                buf[i] = d;
+                if (i == k - 1)
+                    sort_ascending(buf, k); /* Step 2 */
+            } else {
+                oracle_knn_insert(buf, k, d); /* Step 3 */
+            }
+        }
         double sum = 0.0;
         for (int i = 0; i < k; ++i)
             sum += buf[i];
         robs_out[q] = sum / (double)k;
+        if (d1sq_out)
+            d1sq_out[q] = m;
         if (dists_out)
             for (int i = 0; i < k; ++i)
                 dists_out[q * k + i] = buf[i];
@@ -127,21 +149,26 @@ int oracle_knn_f64(const double *x, const double *y, int64_t nd,
  * (PAPER.md:402-405), with the canonical distance sequence of DESIGN.md R16:
  *   dx = qx - px; dy = qy - py; s = fma(dx, dx, dy*dy); d = sqrt(s)  (all float, RN).
  * r_obs = (sum of the ascending float d_i, sequential, in float) / (float)k.
+ * d1sq_out (nullable): [nq] min_i s_i in float (the nearest squared distance).
  */
 int oracle_knn_f32(const float *x, const float *y, int64_t nd,
                    const float *qx, const float *qy, int64_t nq, int k,
-                   float *dists_out, float *robs_out)
+                   float *dists_out, float *robs_out, float *d1sq_out)
 {
     if (k < 1 || k > KMAX || nd < k)
         return -1;
 #pragma omp parallel for schedule(static)
     for (int64_t q = 0; q < nq; ++q) {
         float buf[KMAX];
+        float m = INFINITY;
         for (int64_t i = 0; i < nd; ++i) {
             float dx = qx[q] - x[i];
             float dy = qy[q] - y[i];
             float dy2 = dy * dy;
-            float d = sqrtf(fmaf(dx, dx, dy2));
+            float s = fmaf(dx, dx, dy2);
+            if (s < m)
+                m = s;
+            float d = sqrtf(s);
             if (i < k) {
                 buf[i] = d;
                 if (i == k - 1)
@@ -154,6 +181,8 @@ int oracle_knn_f32(const float *x, const float *y, int64_t nd,
         for (int i = 0; i < k; ++i)
             sum += buf[i];
         robs_out[q] = sum / (float)k;
+        if (d1sq_out)
+            d1sq_out[q] = m;
         if (dists_out)
             for (int i = 0; i < k; ++i)
                 dists_out[q * k + i] = buf[i];
