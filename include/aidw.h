@@ -228,7 +228,8 @@ AIDW_API aidw_status aidw_paper_baseline(int variant, aidw_dtype dt, aidw_layout
  * ranks (shard boundaries at multiples of 1024 points keep the fp32 tile sums identical),
  * every rank evaluates ALL queries against its shard, and the per-shard results are
  * combined exactly (kNN) or in a fixed rank order (Eq. 1 sums).  Sequence per rank:
- *   aidw_set_extent(h, nd_total, area)      r_exp of the WHOLE data set (Eq. 2)
+ *   aidw_set_extent_bbox(h, nd_total, bbox) r_exp of the WHOLE data set (Eq. 2) from
+ *                                           the job-wide bbox (MAX-allreduced aidw_bbox)
  *   aidw_knn_partial -> allgather lists    -> aidw_knn_merge (r_obs, d1sq, {-min, max})
  *   aidw_alpha (GLOBAL: the merged bounds already cover all queries)
  *   aidw_interpolate_partial -> allgather partials -> aidw_finalize (Z)
@@ -239,6 +240,13 @@ AIDW_API aidw_status aidw_set_extent(aidw_t h, int64_t nd_total, double area);
 
 /* Bounding box of the handle's data: out[4] = {min x, max x, min y, max y} (host). */
 AIDW_API aidw_status aidw_bbox(aidw_t h, double *out);
+
+/* Eq. 2 for a data set split across handles: A = (x1 - x0)(y1 - y0)
+ * from the JOB-WIDE bbox[4] = {min x, max x, min y, max y} (host; the MAX-allreduce of
+ * every shard's {-min x, max x, -min y, max y}, R5), in fp64 exactly as
+ * aidw_create computes it for one handle, then r_exp = 1/(2 sqrt(nd_total / A)).
+ * AIDW_E_DEGENERATE_EXTENT if A == 0, AIDW_E_INVALID_AREA if non-finite. */
+AIDW_API aidw_status aidw_set_extent_bbox(aidw_t h, int64_t nd_total, const double *bbox);
 
 /* The k smallest SQUARED distances (ascending) of each query to this handle's data:
  * s_out device T[nq*k].  Same kernel and arithmetic as aidw_knn_robs (R16). */
@@ -269,9 +277,13 @@ AIDW_API aidw_status aidw_finalize(aidw_t h, const double *partials, int P, int6
  * its {-min, max} into every rank's exchange buffer over NVLink (CUDA IPC mappings,
  * system-scope release), and aidw_alpha(GLOBAL, robs_minmax = NULL) waits on the
  * device for all ranks of the same step (acquire loads), then takes the MAX.  Bounds
- * are bit-identical to the allreduce (MAX is exact).  Every rank must call aidw_knn_robs
+ * are bit-identical to the allreduce (MAX is exact).  Values of step e go to slot e mod 2
+ * and each rank acks a step once its alpha launch has read it; a rank publishes step e
+ * only after every rank acked step e - 2, so ranks may drift by one step without a
+ * slower rank ever reading a newer step's bounds.  Every rank must call aidw_knn_robs
  * (with robs_minmax != NULL; nq == 0 pushes the MAX identity) and aidw_alpha in step;
- * a wait gives up after ~2 s and aidw_check then reports it.  One process per GPU;
+ * a wait gives up after ~2 s: alpha (hence Z) of that step is NaN and aidw_check
+ * returns AIDW_E_CUDA.  One process per GPU;
  * processes sharing a GPU also work (tests).  Not for aidw_run_host.
  *   aidw_exchange_setup  : allocate this rank's buffer; ipc_handle_out receives 64 bytes
  *                          (a cudaIpcMemHandle_t) to all-gather across ranks

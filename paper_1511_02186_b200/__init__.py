@@ -44,7 +44,7 @@ EXPORTS = (
     "aidw_abi_version", "aidw_status_string", "aidw_last_error", "aidw_create", "aidw_nd",
     "aidw_area", "aidw_r_exp", "aidw_dtype_of", "aidw_knn_robs", "aidw_alpha", "aidw_interpolate",
     "aidw_run_host", "aidw_check", "aidw_launch_count", "aidw_destroy", "aidw_run_fixed", "aidw_idw",
-    "aidw_paper_baseline", "aidw_set_extent", "aidw_bbox", "aidw_knn_partial", "aidw_knn_merge",
+    "aidw_paper_baseline", "aidw_set_extent", "aidw_set_extent_bbox", "aidw_bbox", "aidw_knn_partial", "aidw_knn_merge",
     "aidw_interpolate_partial", "aidw_finalize", "aidw_exchange_setup", "aidw_exchange_connect",
     "aidw_exchange_close",
 )
@@ -88,6 +88,7 @@ def lib():
             "aidw_paper_baseline": ([I, I, I, P, I64, P, P, I64, I, P, D, D, D, P, P], I),
             "aidw_set_extent": ([P, I64, D], I),
             "aidw_bbox": ([P, P], I),
+            "aidw_set_extent_bbox": ([P, I64, P], I),
             "aidw_knn_partial": ([P, P, P, I64, I, P, P], I),
             "aidw_knn_merge": ([P, P, I, I64, I, P, P, P, P], I),
             "aidw_interpolate_partial": ([P, P, P, I64, P, P, P, P], I),
@@ -119,6 +120,14 @@ def _stream(stream=None, device=None):
     if stream is None:
         stream = torch.cuda.current_stream(device)
     return ctypes.c_void_p(stream.cuda_stream)
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
 
 
 def _levels(levels):
@@ -279,7 +288,10 @@ class AIDW:
             return z
         if rbounds == GLOBAL and group is not None:
             nvtx.range_push("aidw.allreduce_bounds")
-            allreduce_bounds(mm, group)
+            # the collective runs on torch's current stream: make it `stream` so it is
+            # ordered after the kNN that writes mm and before the alpha that reads it
+            with torch.cuda.stream(stream) if stream is not None else _nullctx():
+                allreduce_bounds(mm, group)
             nvtx.range_pop()
         nvtx.range_push("aidw.alpha")
         a = self.alpha(r_obs, levels, rbounds, r_min, r_max, mm, muform, stream)
@@ -316,6 +328,15 @@ class AIDW:
         _err(self.h, lib().aidw_set_extent(self.h, int(nd_total), float(area)))
         self.r_exp = lib().aidw_r_exp(self.h)
         self.area = lib().aidw_area(self.h)
+        self.nd_total = int(nd_total)
+
+    def set_extent_bbox(self, nd_total, bbox):
+        """Eq. 2 for the whole (sharded) data set from the job-wide bbox (aidw_set_extent_bbox)."""
+        b = (ctypes.c_double * 4)(*[float(v) for v in bbox])
+        _err(self.h, lib().aidw_set_extent_bbox(self.h, int(nd_total), b))
+        self.r_exp = lib().aidw_r_exp(self.h)
+        self.area = lib().aidw_area(self.h)
+        self.nd_total = int(nd_total)
 
     def bbox(self):
         out = (ctypes.c_double * 4)()

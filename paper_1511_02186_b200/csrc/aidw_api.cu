@@ -381,7 +381,7 @@ aidw_status aidw_alpha(aidw_t h, const void *r_obs, int64_t nq, const double *al
     if (!r_obs || !alpha) return fail(h, AIDW_E_INVALID_ARG, "r_obs/alpha is NULL");
     CK(h, cudaSetDevice(h->device));
     // GLOBAL with robs_minmax == NULL on a connected handle: bounds from the exchange
-    const aidw::Scratch *ex = (rb == AIDW_RB_GLOBAL && !robs_minmax && h->ex_connected) ? h->sc : nullptr;
+    aidw::Scratch *ex = (rb == AIDW_RB_GLOBAL && !robs_minmax && h->ex_connected) ? h->sc : nullptr;
     return launched(h,
                     aidw::launch_alpha((int)h->dt, r_obs, nq, h->r_exp, alpha_lv, (int)rb, r_min, r_max,
                                        robs_minmax, (int)mf, alpha, static_cast<cudaStream_t>(stream), ex),
@@ -441,6 +441,7 @@ aidw_status aidw_exchange_connect(aidw_t h, const void *ipc_handles)
     sc.ex_world = h->ex_world;
     sc.ex_epoch = 0;
     sc.ex_timeout = 0;
+    sc.ex_readers = 0;
     CK(h, cudaMemcpy(h->sc, &sc, sizeof sc, cudaMemcpyHostToDevice));
     h->ex_connected = true;
     return AIDW_OK;
@@ -595,6 +596,19 @@ aidw_status aidw_set_extent(aidw_t h, int64_t nd_total, double area)
     return AIDW_OK;
 }
 
+aidw_status aidw_set_extent_bbox(aidw_t h, int64_t nd_total, const double *bbox)
+{
+    if (!h || !bbox) return fail(h, AIDW_E_INVALID_ARG, "NULL argument");
+    if (nd_total < 1) return fail(h, AIDW_E_INVALID_ARG, "nd_total must be >= 1");
+    const double area = (bbox[1] - bbox[0]) * (bbox[3] - bbox[2]);  // DESIGN.md R5, as in aidw_create
+    if (std::isnan(area) || std::isinf(area))
+        return fail(h, AIDW_E_INVALID_AREA, "job bbox area = %g is not finite", area);
+    if (!(area > 0.0))
+        return fail(h, AIDW_E_DEGENERATE_EXTENT, "study area A = %g (bbox [%g,%g]x[%g,%g])", area, bbox[0],
+                    bbox[1], bbox[2], bbox[3]);
+    return aidw_set_extent(h, nd_total, area);
+}
+
 aidw_status aidw_bbox(aidw_t h, double *out)
 {
     if (!h || !out) return fail(h, AIDW_E_INVALID_ARG, "NULL argument");
@@ -682,7 +696,7 @@ aidw_status aidw_check(aidw_t h, void *stream)
             const unsigned zero = 0;
             CK(h, cudaMemcpy(&h->sc->ex_timeout, &zero, sizeof zero, cudaMemcpyHostToDevice));
             return fail(h, AIDW_E_CUDA, "bounds exchange: a peer's {-min, max} did not arrive within ~2 s "
-                                        "(ranks out of step?); local bounds were used");
+                                        "(ranks out of step?); alpha and Z of that step are NaN");
         }
     }
     return AIDW_OK;

@@ -40,13 +40,18 @@ struct SplitBuf {
 };
 
 // Device-side GLOBAL-bounds exchange over peer memory (N4 push): every
-// rank owns one ExBuf; rank r's kNN epilogue writes its {-min, max} into val[r] of EVERY
-// rank's buffer (NVLink P2P stores through CUDA-IPC-mapped pointers) and then flag[r] =
-// epoch; the alpha kernel waits until all flags of its own buffer reach the epoch.
+// rank owns one ExBuf.  At epoch e rank r's kNN epilogue writes its {-min, max} into
+// val[e & 1][r] of EVERY rank's buffer (NVLink P2P stores through CUDA-IPC-mapped
+// pointers), then flag[r] = e (release); rank p's alpha kernel waits until every flag
+// of its own buffer reached e, reads slot e & 1, and -- after its last CTA has read --
+// stores ack[p] = e into every rank's buffer.  A publisher writes slot e & 1 only after
+// every rank acked e - 2 (the previous use of that slot), so a rank that runs one epoch
+// ahead never overwrites values a slower peer has not read yet.
 constexpr int kExMaxRanks = 64;
 struct ExBuf {
-    unsigned long long flag[kExMaxRanks];
-    double val[kExMaxRanks][2];
+    unsigned long long flag[kExMaxRanks];  // epoch rank r last published into this buffer
+    unsigned long long ack[kExMaxRanks];   // epoch rank r finished reading (its alpha kernel)
+    double val[2][kExMaxRanks][2];         // [epoch parity][rank] {-min, max}
 };
 
 // Device scratch owned by a handle.
@@ -64,7 +69,7 @@ struct Scratch {
     int ex_rank, ex_world;
     unsigned long long ex_epoch;  // advanced by the kNN epilogue, read by the alpha kernel
     unsigned ex_timeout;          // set when a wait gave up (reported by aidw_check)
-    unsigned pad1;
+    unsigned ex_readers;          // alpha-kernel CTA ticket: the last reader sends the acks
 };
 
 // Spatial (Morton) order of points and queries for the fp32 kNN:
@@ -124,7 +129,7 @@ int launch_minmax_identity(int dtype, void *minmax, cudaStream_t st);
 
 int launch_alpha(int dtype, const void *r_obs, int64_t nq, double r_exp, const double *lv,
                  int rb, double rmin, double rmax, const void *minmax, int mf, void *alpha,
-                 cudaStream_t st, const Scratch *ex_sc = nullptr);
+                 cudaStream_t st, Scratch *ex_sc = nullptr);
 
 // nq == 0 with an active exchange: push the MAX identity so peers do not wait.
 int launch_exchange_push_identity(Scratch *sc, cudaStream_t st);

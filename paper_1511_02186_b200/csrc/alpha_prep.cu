@@ -108,15 +108,18 @@ int launch_prep(int dtype, int layout, const void *src, int64_t nd, int64_t ndp,
 // Eq. 4-6 per query in fp64 (passes.cuh alpha_eq); GLOBAL bounds read on the device.
 // GLOBAL bounds from the peer-memory exchange: thread 0 of each CTA
 // waits until every rank's flag in this rank's ExBuf reached the epoch the preceding kNN
-// epilogue published (acquire loads), then takes the MAX over ranks of {-min, max}.
-// Gives up after ~2 s (a missing peer) and flags ex_timeout for aidw_check.
-__device__ void exchange_wait(const Scratch *sc, double &v0, double &v1)
+// epilogue published (acquire loads), then takes the MAX over ranks of {-min, max} from
+// slot epoch & 1.  The last CTA to have read (ticket) acks the epoch into every rank's
+// buffer, releasing that slot for epoch + 2.  A wait that exceeds ~2 s (a missing peer)
+// sets ex_timeout for aidw_check and makes the bounds NaN, so alpha and Z come out NaN
+// instead of silently using stale bounds.
+__device__ void exchange_wait(Scratch *sc, double &v0, double &v1)
 {
     __shared__ double s0, s1;
     if (threadIdx.x == 0) {
-        const int n = sc->ex_world;
+        const int n = sc->ex_world, me = sc->ex_rank;
         const unsigned long long ep = *reinterpret_cast<const volatile unsigned long long *>(&sc->ex_epoch);
-        const ExBuf *b = sc->ex_peers[sc->ex_rank];
+        const ExBuf *b = sc->ex_peers[me];
         const long long t0 = clock64();
         bool ok = true;
         for (int r = 0; r < n; ++r) {
@@ -132,14 +135,26 @@ __device__ void exchange_wait(const Scratch *sc, double &v0, double &v1)
             }
             if (!ok) break;
         }
-        if (!ok) atomicExch(const_cast<unsigned *>(&sc->ex_timeout), 1u);
         double a0 = -__longlong_as_double(0x7ff0000000000000ll), a1 = a0;
+        const int slot = (int)(ep & 1);
         for (int r = 0; r < n; ++r) {
-            a0 = fmax(a0, b->val[r][0]);
-            a1 = fmax(a1, b->val[r][1]);
+            a0 = fmax(a0, *reinterpret_cast<const volatile double *>(&b->val[slot][r][0]));
+            a1 = fmax(a1, *reinterpret_cast<const volatile double *>(&b->val[slot][r][1]));
+        }
+        if (!ok) {
+            atomicExch(&sc->ex_timeout, 1u);
+            a0 = a1 = __longlong_as_double(0x7ff8000000000000ll);
         }
         s0 = a0;
         s1 = a1;
+        __threadfence();
+        if (atomicAdd(&sc->ex_readers, 1u) == gridDim.x - 1) {  // every CTA has read: ack
+            sc->ex_readers = 0;
+            __threadfence_system();
+            for (int r = 0; r < n; ++r)
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&sc->ex_peers[r]->ack[me]), "l"(ep)
+                             : "memory");
+        }
     }
     __syncthreads();
     v0 = s0;
@@ -149,7 +164,7 @@ __device__ void exchange_wait(const Scratch *sc, double &v0, double &v1)
 template <typename T>
 __global__ void alpha_kernel(const T *__restrict__ robs, int64_t nq, double r_exp, Levels lv, int rb,
                              double rmin, double rmax, const T *__restrict__ mm, int mf,
-                             T *__restrict__ alpha, const Scratch *ex_sc)
+                             T *__restrict__ alpha, Scratch *ex_sc)
 {
     if (rb == 0) {  // GLOBAL: bounds on r_obs -> bounds on R (division is monotone)
         double m0, m1;
@@ -169,7 +184,7 @@ __global__ void alpha_kernel(const T *__restrict__ robs, int64_t nq, double r_ex
 
 int launch_alpha(int dtype, const void *r_obs, int64_t nq, double r_exp, const double *lvp, int rb,
                  double rmin, double rmax, const void *minmax, int mf, void *alpha, cudaStream_t st,
-                 const Scratch *ex_sc)
+                 Scratch *ex_sc)
 {
     Levels lv;
     for (int i = 0; i < 5; ++i) lv.a[i] = lvp[i];

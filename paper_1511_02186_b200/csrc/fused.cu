@@ -138,9 +138,8 @@ __global__ void __launch_bounds__(kBlock) fused_fixed_kernel(const FusedArgs a)
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
         if (!valid[q]) continue;
-        double zq = st2.SWZ[q] / st2.SW[q];
-        if (d1[q] == 0.f) zq = coincident_mean<float>(qx[q], qy[q], a.px, a.py, a.pz, a.nd);  // R19
-        a.z[qid[q]] = (float)zq;
+        write_result<float>(a.z, nullptr, qid[q], st2.SW[q], st2.SWZ[q], d1[q], qx[q], qy[q], a.px, a.py, a.pz,
+                            a.nd, (double)al[q]);  // R19 coincidence, subnormal nearest
     }
 }
 

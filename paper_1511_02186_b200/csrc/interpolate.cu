@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kBlock) interp_kernel(const InterpArgs<T> a)
         for (int q = 0; q < Q; ++q)
             if (valid[q])
                 write_result<T>(a.z, a.partial, base + q * kBlock, SW[q], SWZ[q], d1[q], qx[q], qy[q], a.px, a.py,
-                                a.pz, a.nd);
+                                a.pz, a.nd, -2.0 * (double)c[q]);
     }
 }
 
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(BLOCK, interp_min_blocks(Q) * kBlock / BLOCK)
         for (int q = 0; q < Q; ++q)
             if (valid[q])
                 write_result<float>(a.z, a.partial, qid[q], acc_s[q][threadIdx.x].x, acc_s[q][threadIdx.x].y, d1[q],
-                                    qx[q], qy[q], a.px, a.py, a.pz, a.nd);
+                                    qx[q], qy[q], a.px, a.py, a.pz, a.nd, -2.0 * (double)st.C[q].x);
     }
 }
 
@@ -274,7 +274,8 @@ template <typename T> __global__ void finalize_split_kernel(const InterpArgs<T> 
             SW += v.x;
             SWZ += v.y;
         }
-        write_result<T>(a.z, a.partial, i, SW, SWZ, a.d1sq[i], a.qx[i], a.qy[i], a.px, a.py, a.pz, a.nd);
+        write_result<T>(a.z, a.partial, i, SW, SWZ, a.d1sq[i], a.qx[i], a.qy[i], a.px, a.py, a.pz, a.nd,
+                        (double)(a.alpha ? a.alpha[i] : a.alpha_const));
     }
 }
 

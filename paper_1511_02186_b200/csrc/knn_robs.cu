@@ -41,17 +41,36 @@ template <typename T> struct KnnArgs {
     const int *perm;  // nullable: launch slot i evaluates query perm[i] (spatial order, §4.7)
 };
 
-// Bounds exchange: values into val[rank] of every rank's ExBuf, a
-// system-scope fence, then the flags (release) -- P2P stores over NVLink.
+// Bounds exchange: wait until every rank acked epoch e - 2 (the last
+// use of slot e & 1), values into val[e & 1][rank] of every rank's ExBuf, a system-scope
+// fence, then the flags (release) -- P2P stores over NVLink.  A wait that exceeds ~2 s
+// (a missing peer) sets ex_timeout (aidw_check reports it) and proceeds.
 __device__ __forceinline__ void exchange_push(Scratch *sc, double v0, double v1)
 {
     const unsigned long long ep = sc->ex_epoch + 1;
     sc->ex_epoch = ep;
     const int me = sc->ex_rank, n = sc->ex_world;
+    if (ep > 2) {
+        const ExBuf *own = sc->ex_peers[me];
+        const long long t0 = clock64();
+        for (int r = 0; r < n; ++r) {
+            unsigned long long f;
+            for (;;) {
+                asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(&own->ack[r]) : "memory");
+                if (f + 2 >= ep) break;
+                if (clock64() - t0 > 4000000000ll) {
+                    atomicExch(&sc->ex_timeout, 1u);
+                    break;
+                }
+                __nanosleep(100);
+            }
+        }
+    }
+    const int slot = (int)(ep & 1);
     for (int r = 0; r < n; ++r) {
         ExBuf *b = sc->ex_peers[r];
-        b->val[me][0] = v0;
-        b->val[me][1] = v1;
+        b->val[slot][me][0] = v0;
+        b->val[slot][me][1] = v1;
     }
     __threadfence_system();
     for (int r = 0; r < n; ++r)

@@ -599,14 +599,35 @@ __device__ __forceinline__ double coincident_mean(T qx, T qy, const T *px, const
     return zc / cnt;
 }
 
+// fp32 weighting with a SUBNORMAL nearest squared distance (0 < d1sq < 2^-126; tiny
+// coordinates, or a query ~1e-19 from a data point near the origin): the packed loop's
+// lg2.approx.ftz flushes subnormal s to -inf and its sums are not usable.  Rare; the lane
+// re-evaluates Eq. 1 over global memory in fp64 with the same nearest-scaled weights
+// w = (s / d1sq)^(-alpha/2) (R20), so data-sharded partials stay on one scale.
+__device__ __forceinline__ void tiny_nearest_sums(float qx, float qy, const float *px, const float *py,
+                                                  const float *pz, int64_t nd, double d1, double alpha,
+                                                  double &SW, double &SWZ)
+{
+    SW = 0.0;
+    SWZ = 0.0;
+    for (int64_t i = 0; i < nd; ++i) {
+        const double s = dist_sq((double)qx, (double)qy, (double)px[i], (double)py[i]);
+        const double w = pow(s / d1, -0.5 * alpha);
+        SW += w;
+        SWZ += w * (double)pz[i];
+    }
+}
+
 // Per-query result: Z (Eq. 1, or the coincidence mean R19), or -- in data-sharded mode --
 // this shard's fp64 partials {sum w, sum w z, sum z_coincident, n_coincident}.
 template <typename T>
 __device__ __forceinline__ void write_result(T *z, double *partial, int64_t idx, double SW, double SWZ, T d1, T qx,
-                                             T qy, const T *px, const T *py, const T *pz, int64_t nd)
+                                             T qy, const T *px, const T *py, const T *pz, int64_t nd, double alpha)
 {
     double zc = 0.0, nc = 0.0;
     if (d1 == T(0)) coincident_sums<T>(qx, qy, px, py, pz, nd, zc, nc);
+    if constexpr (sizeof(T) == 4)
+        if (d1 > T(0) && d1 < 0x1p-126f) tiny_nearest_sums(qx, qy, px, py, pz, nd, (double)d1, alpha, SW, SWZ);
     if (partial) {
         partial[4 * idx] = SW;
         partial[4 * idx + 1] = SWZ;

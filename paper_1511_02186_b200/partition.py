@@ -93,7 +93,10 @@ def data_shard(nd: int, rank: int, world: int, align: int = 1024) -> tuple[int, 
 
 
 def global_extent(engine, group=None):
-    """(nd_total, area) of the whole data set from every rank's shard (Eq. 2 inputs)."""
+    """(nd_total, bbox) of the whole data set from every rank's shard: one allreduce(MAX)
+    of {-min x, max x, -min y, max y} (negation carries the minima through the MAX, as
+    for the r_obs bounds) and one allreduce(SUM) of the shard sizes.  Eq. 2's area and
+    r_exp are then computed behind the C ABI (``engine.set_extent_bbox``)."""
     x0, x1, y0, y1 = engine.bbox()
     dev = getattr(engine, "device", torch.device("cpu"))
     t = torch.tensor([-x0, x1, -y0, y1], dtype=torch.float64, device=dev)
@@ -101,8 +104,20 @@ def global_extent(engine, group=None):
     if group is not None and dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
         dist.all_reduce(n, op=dist.ReduceOp.SUM, group=group)
-    t = t.cpu()
-    return int(n.item()), float((t[1] + t[0]) * (t[3] + t[2]))
+    t = t.cpu().tolist()
+    return int(n.item()), [-t[0], t[1], -t[2], t[3]]
+
+
+def check_data_shards(nd_total: int, world: int, k: int, align: int = 1024) -> None:
+    """Raise (identically on every rank, before any collective) if some rank's data shard
+    would hold fewer than max(k, 1) points: a shard needs k real points for its partial
+    kNN list and at least one for its handle.  Use fewer ranks for such small data sets."""
+    for r in range(world):
+        s, e = data_shard(nd_total, r, world, align)
+        if e - s < max(k, 1):
+            raise ValueError(f"data-sharded mode: rank {r} of {world} gets {e - s} of {nd_total} data points "
+                             f"(< k = {k}; shards are whole blocks of {align}); use at most "
+                             f"{max(1, nd_total // max(align, k))} ranks")
 
 
 def _all_gather_cat(x: torch.Tensor, group=None) -> torch.Tensor:
@@ -116,8 +131,10 @@ def _all_gather_cat(x: torch.Tensor, group=None) -> torch.Tensor:
 
 def run_data_sharded(engine, qx, qy, k, levels, rbounds=GLOBAL, r_min=0.0, r_max=2.0, muform=0, group=None):
     """Full AIDW with the data split across ranks; every rank returns Z for ALL queries.
-    `engine` holds this rank's data shard with the global extent set (global_extent)."""
+    `engine` holds this rank's data shard with the global extent set
+    (``engine.set_extent_bbox(*global_extent(engine, group))``)."""
     world = dist.get_world_size(group) if group is not None and dist.is_initialized() else 1
+    check_data_shards(getattr(engine, "nd_total", engine.nd), world, k)
     nq = len(qx)
     s_local = engine.knn_partial(qx, qy, k)
     lists = _all_gather_cat(s_local, group)

@@ -14,6 +14,16 @@ import torch.distributed as dist  # noqa: E402
 import datagen  # noqa: E402
 
 
+STEPS = 4
+
+
+def step_queries(step, qx, qy):
+    """Step 0 = the cloud's queries; later steps shrink them towards a corner so each
+    step's GLOBAL bounds differ."""
+    f = 1.0 - 0.2 * step
+    return qx * f, qy * f
+
+
 def run(rank, world, port, nq_split, out_dir):
     import paper_1511_02186_b200 as P
     from paper_1511_02186_b200.partition import connect_exchange, run_sharded
@@ -25,10 +35,13 @@ def run(rank, world, port, nq_split, out_dir):
     connect_exchange(eng)
     s, e = nq_split[rank], nq_split[rank + 1]
     outs = []
-    for _ in range(3):  # several steps: the epochs advance in lock-step
-        outs.append(run_sharded(eng, qx[s:e], qy[s:e], 10, datagen.ALPHA_LEVELS, P.GLOBAL).cpu().numpy())
+    # several steps with DIFFERENT query batches (so stale bounds would show), enqueued
+    # without a host sync in between: a rank may run a step ahead of its peer
+    for step in range(STEPS):
+        sx, sy = step_queries(step, qx, qy)
+        outs.append(run_sharded(eng, sx[s:e], sy[s:e], 10, datagen.ALPHA_LEVELS, P.GLOBAL))
     eng.check()
-    np.save(os.path.join(out_dir, f"z{rank}.npy"), np.stack(outs))
+    np.save(os.path.join(out_dir, f"z{rank}.npy"), np.stack([o.cpu().numpy() for o in outs]))
     dist.barrier()
     eng.close()
     dist.destroy_process_group()

@@ -111,8 +111,9 @@ class NumpyShardEngine:
     def bbox(self):
         return [self.x.min(), self.x.max(), self.y.min(), self.y.max()]
 
-    def set_extent(self, nd_total, area):
-        self.re = self.o.r_exp(nd_total, area)
+    def set_extent_bbox(self, nd_total, bbox):
+        self.re = self.o.r_exp(nd_total, (bbox[1] - bbox[0]) * (bbox[3] - bbox[2]))
+        self.nd_total = nd_total
 
     def knn_partial(self, qx, qy, k):
         s = (np.asarray(qx)[:, None] - self.x[None]) ** 2 + (np.asarray(qy)[:, None] - self.y[None]) ** 2
@@ -157,7 +158,7 @@ def _worker_data(rank, world, port, out_q):
         x, y, z, qx, qy = datagen.random_cloud(98, 3000, 201)
         s, e = partition.data_shard(len(x), rank, world)
         eng = NumpyShardEngine(x[s:e], y[s:e], z[s:e])
-        eng.set_extent(*partition.global_extent(eng, dist.group.WORLD))
+        eng.set_extent_bbox(*partition.global_extent(eng, dist.group.WORLD))
         zr = partition.run_data_sharded(eng, qx, qy, 10, LV, partition.GLOBAL, group=dist.group.WORLD)
         out_q.put((rank, zr.numpy()))
     finally:
@@ -182,3 +183,13 @@ def test_data_shard_bounds():
             assert b[0][0] == 0 and b[-1][1] == nd
             assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
             assert all(s % 1024 == 0 for s, _ in b)
+
+
+def test_check_data_shards():
+    """Small data sets on many ranks: a clear error before any collective instead of an
+    empty shard (aidw_create needs nd >= 1) or a shard with fewer than k points."""
+    partition.check_data_shards(1024000, 8, 10)
+    partition.check_data_shards(2048, 2, 10)
+    for nd, world in ((5000, 8), (1030, 2), (1, 2)):
+        with pytest.raises(ValueError, match="data-sharded mode"):
+            partition.check_data_shards(nd, world, 10)
