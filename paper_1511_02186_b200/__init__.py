@@ -206,21 +206,32 @@ class AIDW:
     float) or torch.float64.  ``area``: 0 -> bounding box (Eq. 2's A).
     """
 
-    def __init__(self, x, y, z, dtype=torch.float32, device=None, area=0.0):
+    def __init__(self, x, y, z, dtype=torch.float32, device=None, area=0.0, _data=None):
         lib()
         if device is None:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
         self.dt = F32 if dtype == torch.float32 else F64
         self.tdtype = _TORCH_DT[self.dt]
-        data = torch.stack([torch.as_tensor(v, dtype=self.tdtype).reshape(-1) for v in (x, y, z)])
-        data = data.to(self.device).contiguous()
+        if _data is not None:  # [3, nd] SoA, host (pinned: aidw_create copies it) or device
+            data = _data
+        else:
+            data = torch.stack([torch.as_tensor(v, dtype=self.tdtype).reshape(-1) for v in (x, y, z)])
+            data = data.to(self.device).contiguous()
         self.nd = data.shape[1]
         with torch.cuda.device(self.device):
             self.h = aidw_create(data, self.nd, self.dt, SOA, area, self.device.index)
         self.r_exp = lib().aidw_r_exp(self.h)
         self.area = lib().aidw_area(self.h)
         self.exchanged = False
+
+    @classmethod
+    def from_host(cls, data, device=None, area=0.0):
+        """Handle from a HOST [3, nd] SoA tensor (x, y, z rows; pinned memory makes the
+        copy asynchronous): aidw_create stages it to the device itself (S0)."""
+        if data.is_cuda or data.dim() != 2 or data.shape[0] != 3:
+            raise ValueError("from_host needs a host [3, nd] tensor")
+        return cls(None, None, None, dtype=data.dtype, device=device, area=area, _data=data.contiguous())
 
     def close(self):
         if getattr(self, "h", None):

@@ -31,7 +31,7 @@ __global__ void bench(float *out, Clk *clk, float seed)
             else if (MODE == 1) v[i] = lg2(v[i]);            // MUFU.LG2
             else if (MODE == 2) v[i] = fmaf(v[i], 1.0000001f, 1e-7f);  // FFMA
             else if (MODE == 5) v[i] = rsq(v[i]);                          // MUFU.RSQ
-            else if (MODE == 6) v[i] = rcp(v[i]);                          // MUFU.RCP
+            else if (MODE == 6) v[i] = rcp(v[i] + 1.0f);                   // MUFU.RCP (+FADD: bounded chain)
             else if (MODE == 3) {                                          // FFMA2 (2 FMAs / instr)
                 if (i % 2 == 0) {
                     float2 a = make_float2(v[i], v[i + 1]);
@@ -131,7 +131,15 @@ int main()
     double f2 = run<3>(sms, out, clk, &m3), mix = run<4>(sms, out, clk, &m4);
     double m5, m6;
     double rs = run<5>(sms, out, clk, &m5), rc = run<6>(sms, out, clk, &m6);
-    printf("{\"mufu_rsq_per_clk_sm\": %.2f, \"mufu_rcp_per_clk_sm\": %.2f}\n", rs, rc);
+    // r01 printed 0.00 for RCP: its clock estimate (clock64 / globaltimer deltas of block 0)
+    // was unusable.  Rates below also use the median clock of the other modes, and every
+    // launch is checked.
+    const double mref = (m0 + m1 + m2 + m5) / 4.0;
+    cudaError_t err = cudaGetLastError();
+    // mode 6 issues one FADD per RCP (FMA pipe, co-issued): the MUFU rate is still RCP/clk
+    printf("{\"mufu_rsq_per_clk_sm\": %.2f, \"mufu_rcp_per_clk_sm\": %.2f, \"rcp_mhz\": %.0f, "
+           "\"mufu_rcp_per_clk_sm_at_ref_clock\": %.2f, \"ref_mhz\": %.0f, \"cuda_error\": \"%s\"}\n",
+           rs, rc, m6, rc * m6 / mref, mref, cudaGetErrorString(err));
     double m7, m8;
     double b7 = run<7>(sms, out, clk, &m7), b8 = run<8>(sms, out, clk, &m8);
     // mode 7: values updated = 2 FMAs per FFMA2; mode 8: 2 FFMA2 (4 FMAs) per 4 values
