@@ -19,6 +19,7 @@ AIDW_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --
     --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 2 --warmup 3 --no-cpu-baseline \
     --no-f64 > $O/bench_gloo2.json 2> $O/bench_gloo2.err
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/pipe_peaks.cu -o /tmp/pipe_peaks && /tmp/pipe_peaks > $O/pipe_peaks.jsonl 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo tools/knn_loop_bench.cu -o /tmp/knn_loop_bench && timeout 300 /tmp/knn_loop_bench > $O/knn_loop_bench.jsonl 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
     python bench.py --profile --warmup 1 > /dev/null 2>&1
 XM=sm__inst_executed_pipe_xu.sum,sm__inst_executed_pipe_fmaheavy.sum,sm__inst_executed_pipe_fmalite.sum,sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fmalite_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_fp64.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,sm__cycles_active.avg

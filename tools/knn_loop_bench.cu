@@ -1,0 +1,165 @@
+// knn_loop_bench.cu -- microbenchmark of the kNN filter's main loop (passes.cuh
+// knn_f32_tile) in isolation: one smem tile of (cx, cy, pp) read by every
+// CTA, Q queries per thread, 8-point chunks of packed FFMA2 t = pp + A cx + B cy folded
+// into a running 3-input minimum, one warp vote per group of G points (never taken:
+// thr = -inf).  No TMA ring, no rare path, no epilogue -- the achievable pairs/clk/SM of
+// the instruction mix alone, at a chosen number of resident CTAs per SM.
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo tools/knn_loop_bench.cu -o knn_loop_bench
+// Prints one JSON line per variant: pairs per clock per SM and the FMA-pipe fraction
+// (1 FFMA2 = 2 FMA lanes per pair; 128 FMA lanes/clk/SM).
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int TILE = 512;
+constexpr int THREADS = 128;
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float fmin3f(float a, float b, float c)
+{
+    float d;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float opaque(float x)
+{
+    asm volatile("" : "+f"(x));
+    return x;
+}
+
+struct Clk {
+    unsigned long long c0, c1;
+};
+
+// VAR 0: the product loop (3-input min tree per 8 points)
+// VAR 1: 2-input min per couple (more ALU ops)
+// VAR 2: FFMA2 only (t folded into a packed sum: no min; upper bound of the FMA rate)
+template <int Q, int G, int VAR>
+__global__ void __launch_bounds__(THREADS) knn_loop(const float *__restrict__ g, float *out, int reps, Clk *clk)
+{
+    extern __shared__ __align__(16) float sm[];
+    float *scx = sm, *scy = sm + TILE, *spp = sm + 2 * TILE;
+    for (int i = threadIdx.x; i < 3 * TILE; i += THREADS) sm[i] = g[i];
+    __syncthreads();
+    float A[Q], B[Q], thr[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        A[q] = opaque(-2.0f * (0.1f + 0.01f * q + 1e-6f * threadIdx.x));
+        B[q] = opaque(-2.0f * (0.3f - 0.01f * q));
+        thr[q] = opaque(-1e30f);
+    }
+    float acc = 0.f;
+    float2 pacc[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) pacc[q] = make_float2(0.f, 0.f);
+    unsigned long long c0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll 1
+        for (int j = 0; j < TILE; j += G) {
+            float mn[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) mn[q] = 3.0e38f;
+#pragma unroll
+            for (int c = 0; c < G; c += 8) {
+                float cxv[8], cyv[8], ppv[8];
+#pragma unroll
+                for (int h = 0; h < 8; h += 4) {
+                    const float4 CX = *reinterpret_cast<const float4 *>(scx + j + c + h);
+                    const float4 CY = *reinterpret_cast<const float4 *>(scy + j + c + h);
+                    const float4 PP = *reinterpret_cast<const float4 *>(spp + j + c + h);
+                    cxv[h] = CX.x; cxv[h + 1] = CX.y; cxv[h + 2] = CX.z; cxv[h + 3] = CX.w;
+                    cyv[h] = CY.x; cyv[h + 1] = CY.y; cyv[h + 2] = CY.z; cyv[h + 3] = CY.w;
+                    ppv[h] = PP.x; ppv[h + 1] = PP.y; ppv[h + 2] = PP.z; ppv[h + 3] = PP.w;
+                }
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    float t[8];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const float2 tt = ffma2(make_float2(B[q], B[q]), make_float2(cyv[2 * h], cyv[2 * h + 1]),
+                                                ffma2(make_float2(A[q], A[q]), make_float2(cxv[2 * h], cxv[2 * h + 1]),
+                                                      make_float2(ppv[2 * h], ppv[2 * h + 1])));
+                        if (VAR == 2) {
+                            pacc[q] = ffma2(tt, make_float2(1.0f, 1.0f), pacc[q]);
+                        } else {
+                            t[2 * h] = tt.x;
+                            t[2 * h + 1] = tt.y;
+                        }
+                    }
+                    if (VAR == 0)
+                        mn[q] = fmin3f(fmin3f(t[0], t[1], t[2]), fmin3f(t[3], t[4], t[5]), fmin3f(t[6], t[7], mn[q]));
+                    else if (VAR == 1)
+                        mn[q] = fminf(fminf(fminf(t[0], t[1]), fminf(t[2], t[3])),
+                                      fminf(fminf(fminf(t[4], t[5]), fminf(t[6], t[7])), mn[q]));
+                }
+            }
+            bool hit = false;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) hit |= mn[q] <= thr[q];
+            if (__any_sync(0xffffffffu, hit)) acc += 1.f;  // never: thr = -1e30
+        }
+    }
+    unsigned long long c1 = clock64();
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc += pacc[q].x + pacc[q].y;
+    if (acc == 1234.5f) out[0] = acc;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *clk = Clk{c0, c1};
+}
+
+template <int Q, int G, int VAR>
+static void run(const char *name, int ctas_per_sm, const float *g, float *out, Clk *clk, int sms)
+{
+    auto k = knn_loop<Q, G, VAR>;
+    // pad the dynamic smem so at most ctas_per_sm CTAs fit on an SM
+    size_t smem = 3 * TILE * sizeof(float);
+    const size_t per = (227 * 1024) / ctas_per_sm;
+    if (per > smem) smem = per - 1024;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, THREADS, smem);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k);
+    const int reps = 200;
+    const int grid = sms * occ;
+    k<<<grid, THREADS, smem>>>(g, out, reps, clk);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    k<<<grid, THREADS, smem>>>(g, out, reps, clk);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    Clk h;
+    cudaMemcpy(&h, clk, sizeof h, cudaMemcpyDeviceToHost);
+    const double pairs = (double)grid * THREADS * Q * TILE * reps;
+    const double cyc = (double)(h.c1 - h.c0);  // block 0's cycles (all CTAs resident: one wave)
+    const double ppc = pairs / sms / cyc;
+    printf("{\"variant\": \"%s\", \"Q\": %d, \"G\": %d, \"regs\": %d, \"ctas_per_sm\": %d, \"warps_per_sm\": %d, "
+           "\"pairs_per_clk_sm\": %.2f, \"fma_pipe_frac\": %.3f, \"ms\": %.3f, \"mhz\": %.0f, \"err\": \"%s\"}\n",
+           name, Q, G, fa.numRegs, occ, occ * THREADS / 32, ppc, ppc * 2.0 / 128.0, ms, cyc / (ms * 1e3),
+           cudaGetErrorString(cudaGetLastError()));
+}
+
+int main()
+{
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    float *g, *out;
+    Clk *clk;
+    cudaMalloc(&g, 3 * TILE * sizeof(float));
+    cudaMalloc(&out, 4);
+    cudaMalloc(&clk, sizeof(Clk));
+    float h[3 * TILE];
+    for (int i = 0; i < 3 * TILE; ++i) h[i] = 0.001f * (float)(i % 997);
+    cudaMemcpy(g, h, sizeof h, cudaMemcpyHostToDevice);
+    for (int c : {2, 4, 6, 8, 12}) {
+        run<4, 32, 0>("fmin3_q4", c, g, out, clk, sms);
+        run<2, 32, 0>("fmin3_q2", c, g, out, clk, sms);
+        run<8, 32, 0>("fmin3_q8", c, g, out, clk, sms);
+        run<4, 32, 1>("fmin2_q4", c, g, out, clk, sms);
+        run<4, 32, 2>("ffma2_only_q4", c, g, out, clk, sms);
+    }
+    return 0;
+}
