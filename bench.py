@@ -55,7 +55,9 @@ METRIC = metric_name()
 # the method needs 7 FP32 operations (s: 2 sub + mul + fma; exponent fma; two sums)
 # and 2 transcendentals (log2, exp2).  A transcendental costs 1 SFU op, or 8 FMA-pipe
 # ops when evaluated as a polynomial; the best split of the work over the two pipes
-# gives the bound.  Pipe rates: profiles/r01_pipe_peaks.json (measured on B200).
+# gives the bound.  Pipe rates: profiles/r01_pipe_peaks.json (measured on B200; re-measured
+# in round 2, profiles/r02_pipe_peaks.jsonl: MUFU 15.94, FFMA2 122.8 FMA/clk/SM, DFMA 62.7,
+# MUFU.RCP 15.90 -- within 0.9 %).
 WEIGHT_FP32_PER_PAIR = 7
 TRANSC_PER_PAIR = 2
 POLY_FMA_PER_TRANSC = 8
@@ -612,7 +614,7 @@ def main():
                           f"transcendentals per pair (exact-exponent classes: 6-8 FP32 + 1) split optimally "
                           f"between SFU ({MUFU_PER_CLK_SM}/clk) and FMA pipe ({FMA_PER_CLK_SM}/clk, 8 ops per "
                           f"polynomial transcendental), weighted by the class mix; measured pipe rates "
-                          f"profiles/r02_pipe_peaks.json; sm_max_mhz from MEASURED_PEAKS.json",
+                          f"profiles/r01_pipe_peaks.json (r02 re-measure: profiles/r02_pipe_peaks.jsonl); sm_max_mhz from MEASURED_PEAKS.json",
             "class_mix": {c: round(f, 5) for c, f in fr.items()},
             "hbm_gb_per_s": (traffic / (interp_ms / 1e3) / 1e9) if traffic else None,
             "general_clk_per_pair": weight_clk_per_pair(),
@@ -687,7 +689,7 @@ def fp64_roofline(interp_ms, pairs, f_max, clocks):
     return {"bound": "alu", "kernel": "interp_kernel<double> (S5 weighting pass, fp64)",
             "achieved": rate / 1e9, "peak": peak / 1e9, "unit": "Gpair/s", "frac": rate / peak, "traffic": None,
             "peak_basis": f"{N_SM} SM x {f_max / 1e6:.0f} MHz x {DFMA_PER_CLK_SM} FP64 ops/clk/SM "
-                          f"(profiles/r02_pipe_peaks.json) / {DP_ALGO_PER_PAIR} FP64 ops per pair (DESIGN.md §4.9: "
+                          f"(profiles/r01_pipe_peaks.json) / {DP_ALGO_PER_PAIR} FP64 ops per pair (DESIGN.md §4.9: "
                           f"distance 4, log2 to 2^-36 5, exponent 1, exp2 to 2^-36 8, sums 2)",
             "kernel_fp64_ops_per_pair": DP_PER_PAIR,
             "frac_at_measured_clock": (rate / peak) * (f_max / (clocks["sm_mhz"] * 1e6))

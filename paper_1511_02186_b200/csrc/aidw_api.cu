@@ -377,11 +377,13 @@ aidw_status aidw_alpha(aidw_t h, const void *r_obs, int64_t nq, const double *al
     } else if (nq > 0 && !robs_minmax && !h->ex_connected) {
         return fail(h, AIDW_E_INVALID_ARG, "GLOBAL bounds need robs_minmax (or a connected bounds exchange)");
     }
-    if (nq == 0) return AIDW_OK;
-    if (!r_obs || !alpha) return fail(h, AIDW_E_INVALID_ARG, "r_obs/alpha is NULL");
-    CK(h, cudaSetDevice(h->device));
     // GLOBAL with robs_minmax == NULL on a connected handle: bounds from the exchange
     aidw::Scratch *ex = (rb == AIDW_RB_GLOBAL && !robs_minmax && h->ex_connected) ? h->sc : nullptr;
+    // nq == 0 on a connected exchange still launches (one CTA): this rank must read and
+    // ack the step's bounds, or its peers would wait for the ack before step + 2
+    if (nq == 0 && !ex) return AIDW_OK;
+    if (nq > 0 && (!r_obs || !alpha)) return fail(h, AIDW_E_INVALID_ARG, "r_obs/alpha is NULL");
+    CK(h, cudaSetDevice(h->device));
     return launched(h,
                     aidw::launch_alpha((int)h->dt, r_obs, nq, h->r_exp, alpha_lv, (int)rb, r_min, r_max,
                                        robs_minmax, (int)mf, alpha, static_cast<cudaStream_t>(stream), ex),

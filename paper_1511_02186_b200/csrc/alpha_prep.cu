@@ -191,6 +191,7 @@ int launch_alpha(int dtype, const void *r_obs, int64_t nq, double r_exp, const d
     const int threads = 256;
     int64_t blocks = (nq + threads - 1) / threads;
     if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;  // nq == 0 with the exchange: read + ack only
     if (dtype == 0)
         alpha_kernel<float><<<(unsigned)blocks, threads, 0, st>>>(
             (const float *)r_obs, nq, r_exp, lv, rb, rmin, rmax, (const float *)minmax, mf, (float *)alpha, ex_sc);

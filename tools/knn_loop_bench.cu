@@ -34,6 +34,9 @@ struct Clk {
 // VAR 0: the product loop (3-input min tree per 8 points)
 // VAR 1: 2-input min per couple (more ALU ops)
 // VAR 2: FFMA2 only (t folded into a packed sum: no min; upper bound of the FMA rate)
+// VAR 3: scalar FFMA for t (2 per pair, no packing) + the 3-input min tree
+// VAR 4: FFMA2 for t + a direct compare per pair (hit |= t <= thr; FSETP)
+// VAR 5: half the queries packed (FFMA2), half scalar (FFMA), + the min tree
 template <int Q, int G, int VAR>
 __global__ void __launch_bounds__(THREADS) knn_loop(const float *__restrict__ g, float *out, int reps, Clk *clk)
 {
@@ -71,9 +74,16 @@ __global__ void __launch_bounds__(THREADS) knn_loop(const float *__restrict__ g,
                     cyv[h] = CY.x; cyv[h + 1] = CY.y; cyv[h + 2] = CY.z; cyv[h + 3] = CY.w;
                     ppv[h] = PP.x; ppv[h + 1] = PP.y; ppv[h + 2] = PP.z; ppv[h + 3] = PP.w;
                 }
+                bool hitv = false;
 #pragma unroll
                 for (int q = 0; q < Q; ++q) {
                     float t[8];
+                    if (VAR == 3 || (VAR == 5 && q >= Q / 2)) {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) t[e] = fmaf(B[q], cyv[e], fmaf(A[q], cxv[e], ppv[e]));
+                        mn[q] = fmin3f(fmin3f(t[0], t[1], t[2]), fmin3f(t[3], t[4], t[5]), fmin3f(t[6], t[7], mn[q]));
+                        continue;
+                    }
 #pragma unroll
                     for (int h = 0; h < 4; ++h) {
                         const float2 tt = ffma2(make_float2(B[q], B[q]), make_float2(cyv[2 * h], cyv[2 * h + 1]),
@@ -86,12 +96,17 @@ __global__ void __launch_bounds__(THREADS) knn_loop(const float *__restrict__ g,
                             t[2 * h + 1] = tt.y;
                         }
                     }
-                    if (VAR == 0)
+                    if (VAR == 4) {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) hitv |= t[e] <= thr[q];
+                    }
+                    if (VAR == 0 || VAR == 5)
                         mn[q] = fmin3f(fmin3f(t[0], t[1], t[2]), fmin3f(t[3], t[4], t[5]), fmin3f(t[6], t[7], mn[q]));
                     else if (VAR == 1)
                         mn[q] = fminf(fminf(fminf(t[0], t[1]), fminf(t[2], t[3])),
                                       fminf(fminf(fminf(t[4], t[5]), fminf(t[6], t[7])), mn[q]));
                 }
+                if (VAR == 4) mn[0] = hitv ? -1.0f : mn[0];
             }
             bool hit = false;
 #pragma unroll
@@ -106,10 +121,55 @@ __global__ void __launch_bounds__(THREADS) knn_loop(const float *__restrict__ g,
     if (blockIdx.x == 0 && threadIdx.x == 0) *clk = Clk{c0, c1};
 }
 
+// VAR 6 (separate kernel): lanes = POINTS, the CTA's Q queries uniform across the CTA
+// (coefficients from blockIdx only -> uniform registers): per couple of points 3 LDS.64,
+// per query 2 FFMA2 with a uniform scalar operand and 1 FMNMX3 (min of the couple and
+// the running minimum).
 template <int Q, int G, int VAR>
-static void run(const char *name, int ctas_per_sm, const float *g, float *out, Clk *clk, int sms)
+__global__ void __launch_bounds__(THREADS) knn_loop_uni(const float *__restrict__ g, float *out, int reps, Clk *clk)
 {
-    auto k = knn_loop<Q, G, VAR>;
+    extern __shared__ __align__(16) float sm[];
+    float *scx = sm, *scy = sm + TILE, *spp = sm + 2 * TILE;
+    for (int i = threadIdx.x; i < 3 * TILE; i += THREADS) sm[i] = g[i];
+    __syncthreads();
+    float A[Q], B[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        A[q] = -2.0f * (0.1f + 0.01f * q + 1e-6f * blockIdx.x);
+        B[q] = -2.0f * (0.3f - 0.01f * q - 1e-6f * blockIdx.x);
+    }
+    const float thr = -1e30f;
+    float acc = 0.f;
+    unsigned long long c0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+        float mn[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) mn[q] = 3.0e38f;
+#pragma unroll 1
+        for (int j = 2 * threadIdx.x; j < TILE; j += 2 * THREADS) {
+            const float2 cx = *reinterpret_cast<const float2 *>(scx + j);
+            const float2 cy = *reinterpret_cast<const float2 *>(scy + j);
+            const float2 pp = *reinterpret_cast<const float2 *>(spp + j);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const float2 t = ffma2(make_float2(B[q], B[q]), cy, ffma2(make_float2(A[q], A[q]), cx, pp));
+                mn[q] = fmin3f(t.x, t.y, mn[q]);
+            }
+        }
+        bool hit = false;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) hit |= mn[q] <= thr;
+        if (__any_sync(0xffffffffu, hit)) acc += 1.f;
+    }
+    unsigned long long c1 = clock64();
+    if (acc == 1234.5f) out[0] = acc;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *clk = Clk{c0, c1};
+}
+
+template <int Q, int G, int VAR>
+static void run(const char *name, int ctas_per_sm, const float *g, float *out, Clk *clk, int sms, double mhz_ref)
+{
+    auto k = VAR == 6 ? knn_loop_uni<Q, G, VAR> : knn_loop<Q, G, VAR>;
     // pad the dynamic smem so at most ctas_per_sm CTAs fit on an SM
     size_t smem = 3 * TILE * sizeof(float);
     const size_t per = (227 * 1024) / ctas_per_sm;
@@ -134,11 +194,12 @@ static void run(const char *name, int ctas_per_sm, const float *g, float *out, C
     Clk h;
     cudaMemcpy(&h, clk, sizeof h, cudaMemcpyDeviceToHost);
     const double pairs = (double)grid * THREADS * Q * TILE * reps;
-    const double cyc = (double)(h.c1 - h.c0);  // block 0's cycles (all CTAs resident: one wave)
-    const double ppc = pairs / sms / cyc;
+    // rate from the event time at the SM clock read during the run (block 0's clock64
+    // span is not the kernel's: r02a showed CTAs finishing at different times)
+    const double ppc = pairs / sms / (ms * 1e-3) / (mhz_ref * 1e6);
     printf("{\"variant\": \"%s\", \"Q\": %d, \"G\": %d, \"regs\": %d, \"ctas_per_sm\": %d, \"warps_per_sm\": %d, "
-           "\"pairs_per_clk_sm\": %.2f, \"fma_pipe_frac\": %.3f, \"ms\": %.3f, \"mhz\": %.0f, \"err\": \"%s\"}\n",
-           name, Q, G, fa.numRegs, occ, occ * THREADS / 32, ppc, ppc * 2.0 / 128.0, ms, cyc / (ms * 1e3),
+           "\"pairs_per_clk_sm\": %.2f, \"fma_lanes_frac\": %.3f, \"ms\": %.3f, \"mhz\": %.0f, \"err\": \"%s\"}\n",
+           name, Q, G, fa.numRegs, occ, occ * THREADS / 32, ppc, ppc * 2.0 / 128.0, ms, mhz_ref,
            cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -154,12 +215,21 @@ int main()
     float h[3 * TILE];
     for (int i = 0; i < 3 * TILE; ++i) h[i] = 0.001f * (float)(i % 997);
     cudaMemcpy(g, h, sizeof h, cudaMemcpyHostToDevice);
-    for (int c : {2, 4, 6, 8, 12}) {
-        run<4, 32, 0>("fmin3_q4", c, g, out, clk, sms);
-        run<2, 32, 0>("fmin3_q2", c, g, out, clk, sms);
-        run<8, 32, 0>("fmin3_q8", c, g, out, clk, sms);
-        run<4, 32, 1>("fmin2_q4", c, g, out, clk, sms);
-        run<4, 32, 2>("ffma2_only_q4", c, g, out, clk, sms);
+    int clk_khz = 0;
+    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+    const double mhz = clk_khz / 1e3;  // max SM clock (the runs are checked against nvidia-smi)
+    for (int c : {4, 8}) {
+        run<4, 32, 0>("fmin3_q4", c, g, out, clk, sms, mhz);
+        run<8, 32, 0>("fmin3_q8", c, g, out, clk, sms, mhz);
+        run<4, 32, 1>("fmin2_q4", c, g, out, clk, sms, mhz);
+        run<4, 32, 2>("ffma2_only_q4", c, g, out, clk, sms, mhz);
+        run<4, 32, 3>("scalar_ffma_fmin3_q4", c, g, out, clk, sms, mhz);
+        run<4, 32, 4>("ffma2_fsetp_q4", c, g, out, clk, sms, mhz);
+        run<4, 32, 5>("half_packed_fmin3_q4", c, g, out, clk, sms, mhz);
+        run<8, 32, 5>("half_packed_fmin3_q8", c, g, out, clk, sms, mhz);
+        run<8, 32, 6>("uniform_queries_q8", c, g, out, clk, sms, mhz);
+        run<16, 32, 6>("uniform_queries_q16", c, g, out, clk, sms, mhz);
+        run<32, 32, 6>("uniform_queries_q32", c, g, out, clk, sms, mhz);
     }
     return 0;
 }
