@@ -501,7 +501,7 @@ aidw_status aidw_interpolate(aidw_t h, const void *qx, const void *qy, int64_t n
     aidw::SplitBuf *sp = split_for(h, nq);
     return launched(h,
                     aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, alpha, 0.0, d1sq, z_out, st,
-                                        nullptr, perm_for(h, nq), h->sc->cls, sp),
+                                        nullptr, perm_for(h, nq), h->sc->cls, sp, h->bbox),
                     "interpolate kernel");
 }
 
@@ -563,7 +563,7 @@ aidw_status aidw_idw(aidw_t h, const void *qx, const void *qy, int64_t nq, doubl
     aidw::SplitBuf *sp = split_for(h, nq);
     return launched(h,
                     aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, nullptr, alpha, w + nb,
-                                        z_out, st, nullptr, perm_for(h, nq), h->sc->cls, sp),
+                                        z_out, st, nullptr, perm_for(h, nq), h->sc->cls, sp, h->bbox),
                     "interpolate kernel");
 }
 
@@ -662,7 +662,7 @@ aidw_status aidw_interpolate_partial(aidw_t h, const void *qx, const void *qy, i
     return launched(h,
                     aidw::launch_interp((int)h->dt, h->data, h->ndp, h->nd, qx, qy, nq, alpha, 0.0, d1sq, nullptr,
                                         static_cast<cudaStream_t>(stream), partial_out, perm_for(h, nq),
-                                        h->sc->cls, sp),
+                                        h->sc->cls, sp, h->bbox),
                     "interpolate partial kernel");
 }
 

@@ -151,7 +151,7 @@ int launch_paper(int variant, int dtype, int layout, const void *data, int64_t n
 int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const void *qx,
                   const void *qy, int64_t nq, const void *alpha, double alpha_const, const void *d1sq, void *z,
                   cudaStream_t st, double *partial = nullptr, int *perm = nullptr,
-                  unsigned *cls_counts = nullptr, SplitBuf *split = nullptr);
+                  unsigned *cls_counts = nullptr, SplitBuf *split = nullptr, const double *bbox = nullptr);
 
 // Data-split factor for a launch of `grid` CTAs (small nq fills the GPU by splitting the
 // data range across blockIdx.y); 1 = no split.

@@ -15,6 +15,8 @@
 // Q queries per thread, every data point read once from smem per Q pairs.
 #include "passes.cuh"
 
+#include <limits>
+
 #include <cstdlib>
 
 namespace aidw {
@@ -29,7 +31,23 @@ template <typename T> struct InterpArgs {
     double *partial;  // nullable: data-sharded partial sums instead of z
     const int *perm;  // nullable: position i evaluates query perm[i] (class grouping)
     double2 *bpart;   // split mode: per-accumulation-block sums [nblk][nq] (gridDim.y > 1)
+    float bb[4];      // data bbox {x0, x1, y0, y1} (fp32 kernel's clamp-free test); NaN: unknown
 };
+
+// fp32 general formula without the exp2 clamp (round 2): a query's
+// exponents e = c lg2(s) + b over its REAL data points are >= c lg2(s_max) + b, s_max the
+// squared distance to the farthest bbox corner (c < 0).  When that bound is >= -120 the
+// polynomial exp2's clamp to -126 never fires, so dropping it (2 FMNMX per couple) leaves
+// every weight bit-identical.  Coincident (d1 = 0), subnormal-nearest and far-outside
+// queries fail the test and keep the clamp, as do the tiles holding padding points.
+__device__ __forceinline__ bool exp2_clamp_free(float qx, float qy, float alpha, float d1sq, const float (&bb)[4])
+{
+    const float dxm = fmaxf(fabsf(qx - bb[0]), fabsf(qx - bb[1]));
+    const float dym = fmaxf(fabsf(qy - bb[2]), fabsf(qy - bb[3]));
+    const float smax = __fmul_ru(__fmaf_ru(dxm, dxm, __fmul_ru(dym, dym)), 1.0001f);
+    const float e = 0.5f * alpha * (lg2_approx_noftz(d1sq) - lg2_approx_noftz(smax));
+    return e >= -120.0f;  // false for NaN / -inf (coincident, unknown bbox, overflow)
+}
 
 // Weight math per precision: fp32 MUFU (scalar variant), fp64 table + polynomial
 // (passes.cuh log2_f64 / exp2_f64; tables staged in shared memory).
@@ -211,6 +229,16 @@ __global__ void __launch_bounds__(BLOCK, interp_min_blocks(Q) * kBlock / BLOCK)
         cls[q] = a.perm ? alpha_class(al, d1[q]) : kClsGeneral;
         if (valid[q]) present |= 1u << cls[q];
     }
+    // the exp2 clamp is needed only for queries whose far weights may drop below 2^-126
+    // and on tiles holding padding points (s = +inf)
+    bool unsafe = false;
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+        if (valid[q])
+            unsafe |= !exp2_clamp_free(qx[q], qy[q], -2.0f * st.C[q].x, d1[q], a.bb);
+    // tiles from clamp_from on use the clamped exp2: all of them if some query needs it,
+    // else those holding padding points
+    const int clamp_from = __syncthreads_or(unsafe) ? 0 : (int)(a.nd / TILE);
     int cta_cls = kClsGeneral;
     if (a.perm) {
         const int any_g = __syncthreads_or(present & 1u), any_1 = __syncthreads_or(present & 2u);
@@ -231,7 +259,12 @@ __global__ void __launch_bounds__(BLOCK, interp_min_blocks(Q) * kBlock / BLOCK)
         case kClsA2: interp_f32_tile_cls<Q, kClsA2, EMU, TILE>(st, cls, r.sx + o, r.sy + o, r.sz + o); break;
         case kClsA3: interp_f32_tile_cls<Q, kClsA3, EMU, TILE>(st, cls, r.sx + o, r.sy + o, r.sz + o); break;
         case kClsMixed: interp_f32_tile_cls<Q, kClsMixed, EMU, TILE>(st, cls, r.sx + o, r.sy + o, r.sz + o); break;
-        default: interp_f32_tile<Q, EMU, TILE>(st, r.sx + o, r.sy + o, r.sz + o); break;
+        default:
+            if (t0 + t >= clamp_from)
+                interp_f32_tile<Q, EMU, TILE, true>(st, r.sx + o, r.sy + o, r.sz + o);
+            else
+                interp_f32_tile<Q, EMU, TILE, false>(st, r.sx + o, r.sy + o, r.sz + o);
+            break;
         }
         if (t + 1 == bend) {  // end of an accumulation block
             if constexpr (SPLIT) {
@@ -485,6 +518,9 @@ static int launch_interp_f32(const InterpArgs<float> &a, cudaStream_t st, SplitB
     case 33: return launch_interp_f32x2<2, 0x4105>(a, st, sp);  // Q = 2, f = 4/8 (0, 1, 4, 7)
     case 34: return launch_interp_f32x2<2, 0x0141>(a, st, sp);  // Q = 2, f = 3/8
     case 35: return launch_interp_f32x2<1, 0x0141>(a, st, sp);  // Q = 1, f = 3/8 (default before v10)
+    case 36: return launch_interp_f32x2<2, 0x4151>(a, st, sp);  // Q = 2, f = 5/8 spread (r02)
+    case 37: return launch_interp_f32x2<2, 0x5151>(a, st, sp);  // Q = 2, f = 6/8 spread (r02)
+    case 38: return launch_interp_f32x2<2, 0x4241>(a, st, sp);  // Q = 2, f = 9/16 (one split couple, r02)
     default: break;
     }
     // Q = 2, f = 4/8 spread (best measured, r01 v10); a grid of fewer than ~5 waves even
@@ -523,15 +559,26 @@ int launch_finalize(int dtype, const double *partials, int P, int64_t nq, void *
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
+// Tuning/testing switch read per launch: the integer value of env var `name`, -1 if unset.
+static int getenv_flag(const char *name)
+{
+    const char *e = getenv(name);
+    return e ? atoi(e) : -1;
+}
+
 int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const void *qx,
                   const void *qy, int64_t nq, const void *alpha, double alpha_const, const void *d1sq, void *z,
-                  cudaStream_t st, double *partial, int *perm, unsigned *cls_counts, SplitBuf *split)
+                  cudaStream_t st, double *partial, int *perm, unsigned *cls_counts, SplitBuf *split,
+                  const double *bbox)
 {
     if (dtype == 0) {
         const float *p = static_cast<const float *>(data);
         InterpArgs<float> a{p, p + ndp, p + 2 * ndp, ndp, nd, (const float *)qx, (const float *)qy,
                             (const float *)alpha, (const float *)d1sq, nq, (float *)z, (float)alpha_const,
                             partial, nullptr, nullptr};
+        const bool clamp_free = bbox && getenv_flag("AIDW_EXP2_CLAMP") != 1;
+        for (int i = 0; i < 4; ++i)  // fp32 data: the bbox is exact in fp32
+            a.bb[i] = clamp_free ? (float)bbox[i] : std::numeric_limits<float>::quiet_NaN();
         int launches = 0;
         if (perm && cls_counts && interp_variant() != 1) {
             if (cudaMemsetAsync(cls_counts, 0, 8 * sizeof(unsigned), st) != cudaSuccess) return -1;
@@ -549,7 +596,7 @@ int launch_interp(int dtype, const void *data, int64_t ndp, int64_t nd, const vo
     const double *p = static_cast<const double *>(data);
     InterpArgs<double> a{p, p + ndp, p + 2 * ndp, ndp, nd, (const double *)qx, (const double *)qy,
                          (const double *)alpha, (const double *)d1sq, nq, (double *)z, alpha_const, partial,
-                         nullptr, nullptr};
+                         nullptr, nullptr, {0.f, 0.f, 0.f, 0.f}};
     if (small_grid(nq, ndp, 8)) return launch_interp_t<double, 1>(a, st, split);
     return launch_interp_t<double, 2>(a, st, split);
 }

@@ -26,13 +26,19 @@ __device__ __forceinline__ f32x2 splat2(float v) { return make_float2(v, v); }
 // tools/fit_exp2.py), exponent added as an integer: bits(2^f) + (j << 23).
 // Results below 2^-126 are not produced (the clamp): such weights are < 1e-38 of the
 // nearest point's weight (w is scaled to 1 at the nearest point) and vanish in the sums.
+// CLAMP = false: the caller guarantees x >= -126 (round 2: tiles without
+// padding points, CTAs whose queries' weights provably stay above 2^-126), saving the two
+// FMNMX per couple; the result is then bit-identical to the clamped form.
+template <bool CLAMP = true>
 __device__ __forceinline__ f32x2 exp2_poly2(f32x2 a)
 {
     constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
     float a0, a1;
     unpack2(a, a0, a1);
-    a0 = fmaxf(a0, -126.0f);
-    a1 = fmaxf(a1, -126.0f);
+    if (CLAMP) {
+        a0 = fmaxf(a0, -126.0f);
+        a1 = fmaxf(a1, -126.0f);
+    }
     const f32x2 x = pack2(a0, a1);
     const f32x2 t = add2(x, splat2(kMagic));
     const f32x2 j = sub2(t, splat2(kMagic));
@@ -50,10 +56,11 @@ __device__ __forceinline__ f32x2 exp2_poly2(f32x2 a)
 }
 
 // Scalar form of exp2_poly2 (same constants and operation order, per element).
+template <bool CLAMP = true>
 __device__ __forceinline__ float exp2_poly1(float a)
 {
     constexpr float kMagic = 12582912.0f;
-    const float x = fmaxf(a, -126.0f);
+    const float x = CLAMP ? fmaxf(a, -126.0f) : a;
     const float t = __fadd_rn(x, kMagic);
     const float j = __fadd_rn(t, -kMagic);
     const float f = __fadd_rn(x, -j);

@@ -413,7 +413,7 @@ struct InterpF32State {
 // tile sums are {even, odd} partial sums folded into fp64 at the end of the tile (R21).
 // The ex2 of couple (q, h) runs on the FMA pipe (exp2_poly2) when bit 2q+h of EMU is
 // set, on the SFU otherwise.
-template <int Q, unsigned HMASK>
+template <int Q, unsigned HMASK, bool CLAMP = true>
 __device__ __forceinline__ void interp_f32_group(InterpF32State<Q> &st, f32x2 (&sw)[Q], f32x2 (&swz)[Q],
                                                  const float *__restrict__ tx, const float *__restrict__ ty,
                                                  const float *__restrict__ tz)
@@ -436,9 +436,9 @@ __device__ __forceinline__ void interp_f32_group(InterpF32State<Q> &st, f32x2 (&
             f32x2 w;
             const unsigned m = (HMASK >> (2 * h)) & 3u;
             if (m == 1u)
-                w = exp2_poly2(e);  // both lanes on the FMA pipe (packed)
+                w = exp2_poly2<CLAMP>(e);  // both lanes on the FMA pipe (packed)
             else if (m == 2u)
-                w = pack2(ex2_approx(e.x), exp2_poly1(e.y));  // split: SFU + FMA pipe
+                w = pack2(ex2_approx(e.x), exp2_poly1<CLAMP>(e.y));  // split: SFU + FMA pipe
             else
                 w = pack2(ex2_approx(e.x), ex2_approx(e.y));
             sw[q] = add2(sw[q], w);
@@ -455,7 +455,7 @@ __device__ __forceinline__ void interp_f32_group(InterpF32State<Q> &st, f32x2 (&
 // (DESIGN.md §4.3).  The choice depends on the data-point index only -- never on which register
 // slot holds the query -- so every query's rounding is independent of its position in
 // the launch (bit-identical results for any sharding).
-template <int Q, unsigned EMU, int TILE>
+template <int Q, unsigned EMU, int TILE, bool CLAMP = true>
 __device__ __forceinline__ void interp_f32_tile(InterpF32State<Q> &st, const float *__restrict__ tx,
                                                 const float *__restrict__ ty, const float *__restrict__ tz)
 {
@@ -465,10 +465,10 @@ __device__ __forceinline__ void interp_f32_tile(InterpF32State<Q> &st, const flo
     for (int q = 0; q < Q; ++q) sw[q] = swz[q] = make_float2(0.f, 0.f);
 #pragma unroll 1
     for (int j = 0; j < TILE; j += 16) {
-        interp_f32_group<Q, (EMU >> 0) & 15u>(st, sw, swz, tx + j, ty + j, tz + j);
-        interp_f32_group<Q, (EMU >> 4) & 15u>(st, sw, swz, tx + j + 4, ty + j + 4, tz + j + 4);
-        interp_f32_group<Q, (EMU >> 8) & 15u>(st, sw, swz, tx + j + 8, ty + j + 8, tz + j + 8);
-        interp_f32_group<Q, (EMU >> 12) & 15u>(st, sw, swz, tx + j + 12, ty + j + 12, tz + j + 12);
+        interp_f32_group<Q, (EMU >> 0) & 15u, CLAMP>(st, sw, swz, tx + j, ty + j, tz + j);
+        interp_f32_group<Q, (EMU >> 4) & 15u, CLAMP>(st, sw, swz, tx + j + 4, ty + j + 4, tz + j + 4);
+        interp_f32_group<Q, (EMU >> 8) & 15u, CLAMP>(st, sw, swz, tx + j + 8, ty + j + 8, tz + j + 8);
+        interp_f32_group<Q, (EMU >> 12) & 15u, CLAMP>(st, sw, swz, tx + j + 12, ty + j + 12, tz + j + 12);
     }
 #pragma unroll
     for (int q = 0; q < Q; ++q) {

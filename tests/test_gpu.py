@@ -233,6 +233,25 @@ def test_coincident_queries(P, orc, dtype):
     assert np.allclose(Zg[64:69], (z[:5] + z[5:10]) / 2, rtol=TOL[dtype])
 
 
+@pytest.mark.parametrize("nd,nq", [(3000, 777), (100003, 20000), (262144, 65536)])
+def test_exp2_clamp_free_bit_identical(P, monkeypatch, nd, nq):
+    """The fp32 weighting pass drops the polynomial exp2's clamp on tiles without padding
+    points for CTAs whose weights provably stay above 2^-126 (interpolate.cu
+    exp2_clamp_free): Z is bit-identical to the always-clamped kernel (AIDW_EXP2_CLAMP=1),
+    with coincident queries (which keep the clamp) and queries far outside the data."""
+    x, y, z, qx, qy = datagen.random_cloud(nd + nq, nd, nq)
+    qx[::97], qy[::97] = x[: len(qx[::97])], y[: len(qy[::97])]  # coincident
+    qx[5], qy[5] = 40.0, -25.0  # far outside
+    eng = P.AIDW(x, y, z)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("AIDW_EXP2_CLAMP", flag)
+        out[flag] = [eng.run(qx, qy, 10, LV, m).cpu().numpy() for m in (P.GLOBAL, P.FIXED)]
+        out[flag].append(eng.idw(qx, qy, 2.5).cpu().numpy())
+    for a, b in zip(out["1"], out["0"]):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 def test_subnormal_nearest_distance(P, orc, dtype):
     """A query ~1e-21 from a data point near the origin: its nearest squared distance is
