@@ -316,10 +316,14 @@ template <typename T> __host__ __device__ constexpr int filter_arrays() { return
 
 // SPLIT: 0 = whole data range; 1 = a split (seeded from the home tile when the batch is
 // spatially ordered); 2 = an unordered split with the per-query seed (seed_query).
-template <typename T, int K, int Q, int G, int SPLIT, int MINB = 0>
+// H16: fp32 handles, spatially ordered batches -- the fp16 pre-filter (passes.cuh
+// knn_h16_tile) replaces the fp32 main loop once every query of the CTA has a finite
+// k-th distance (after the seed tile, or the first tile).
+template <typename T, int K, int Q, int G, int SPLIT, int MINB = 0, bool H16 = false>
 __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<T> a, const FilterArgs f)
 {
     constexpr int TILE = kTileKF, STAGES = kStagesKF, NARR = filter_arrays<T>();
+    static_assert(!H16 || NARR == 5, "the fp16 pre-filter is for fp32 handles");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float *scx = reinterpret_cast<float *>(smem_raw);
     float *scy = scx + STAGES * TILE;
@@ -391,16 +395,98 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
         }
     }
 
+    // fp16 pre-filter state (H16): the CTA's query-bbox centre, the scale, per-query
+    // coefficients and thresholds; enabled once every query has a finite k-th distance
+    __shared__ __align__(16) __half2 hbuf[H16 ? 2 : 1][3][H16 ? TILE / 2 : 1];
+    __shared__ unsigned hred[4];
+    KnnH16<Q> h16;
+    float Cx = 0.f, Cy = 0.f, sig = 0.f;
+    bool h16_on = false;
+    if constexpr (H16) {
+        // centre of the CTA's valid queries (order-preserving keys of the fp32 values)
+        auto key = [](float v) { const unsigned b = __float_as_uint(v); return (b >> 31) ? ~b : b | 0x80000000u; };
+        auto unkey = [](unsigned k) { return __uint_as_float((k >> 31) ? k & 0x7fffffffu : ~k); };
+        if (threadIdx.x == 0) hred[0] = hred[2] = 0xffffffffu, hred[1] = hred[3] = 0u;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            if (valid[q] && isfinite(qx[q]) && isfinite(qy[q])) {
+                atomicMin(&hred[0], key(qx[q]));
+                atomicMax(&hred[1], key(qx[q]));
+                atomicMin(&hred[2], key(qy[q]));
+                atomicMax(&hred[3], key(qy[q]));
+            }
+        __syncthreads();
+        if (hred[0] != 0xffffffffu) {
+            Cx = 0.5f * unkey(hred[0]) + 0.5f * unkey(hred[1]);
+            Cy = 0.5f * unkey(hred[2]) + 0.5f * unkey(hred[3]);
+        }
+        __syncthreads();  // hred is reused for the scale
+    }
+
     for (int t = 0; t < ntiles; ++t) {
         ring.wait_full(t);
         const int o = ring.slot(t) * TILE;
-        if constexpr (NARR == 5) {
+        if constexpr (H16) {
+            if (h16_on) {
+                __half2 *hb = &hbuf[t & 1][0][0];
+                h16_convert<TILE>(spx + o, spy + o, hb, hb + TILE / 2, hb + TILE, Cx, Cy, sig);
+                __syncthreads();
+                knn_h16_tile<K, Q, G, TILE>(st, h16, hb, hb + TILE / 2, hb + TILE, scx + o, scy + o, spp + o,
+                                            spx + o, spy + o, Cx, Cy, sig);
+            } else {  // warm-up tile (lists not yet finite): every group straight to the rare
+                      // path -- with an infinite threshold the filter passes every pair anyway --
+                      // so the kernel carries no fp32 main loop (registers)
+                bool all[Q];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) all[q] = true;
+#pragma unroll 1
+                for (int j = 0; j < TILE; j += G)
+                    knn_rare_group<K, Q, G>(st, all, scx + o, scy + o, spp + o, spx + o, spy + o, j);
+            }
+        } else if constexpr (NARR == 5) {
             knn_f32_tile<K, Q, G, TILE>(st, scx + o, scy + o, spp + o, spx + o, spy + o);
         } else {
             const int64_t off = (int64_t)tile_of(t) * TILE;
             knn_f32_tile<K, Q, G, TILE, T>(st, scx + o, scy + o, spp + o, f.px64 + off, f.py64 + off);
         }
         if (seed && t == 0) st.seed_lists(k0);  // home tile scanned: lists := seed copies
+        if constexpr (H16) {
+            if (!h16_on && t + 1 < ntiles) {  // every list finite: fix the scale, switch to fp16
+                bool fin = true;
+#pragma unroll
+                for (int q = 0; q < Q; ++q) fin &= !valid[q] || st.buf[q][K - 1] < pos_inf<float>();
+                if (__syncthreads_and(fin)) {
+                    float m = 0.f;  // largest |q - C| and k-th distance over the CTA (non-negative)
+#pragma unroll
+                    for (int q = 0; q < Q; ++q)
+                        if (valid[q]) {
+                            const float dx = qx[q] - Cx, dy = qy[q] - Cy;
+                            m = fmaxf(m, fmaxf(sqrtf(dx * dx + dy * dy), sqrtf((float)st.buf[q][K - 1])));
+                        }
+                    if (threadIdx.x == 0) hred[0] = 0u;
+                    __syncthreads();
+                    atomicMax(&hred[0], __float_as_uint(m * 1.001f));
+                    __syncthreads();
+                    const float mm = __uint_as_float(hred[0]);
+                    int e = 0;
+                    frexpf(kH16Radius / fmaxf(mm, 0x1p-100f), &e);  // 16/m = f 2^e, f in [0.5, 1)
+                    e = e - 1 < -100 ? -100 : (e - 1 > 100 ? 100 : e - 1);
+                    sig = ldexpf(1.0f, e);  // sigma m <= 16
+                    h16_on = isfinite(mm) && sig > 0.f && isfinite(sig);
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
+                        const float ax = -2.0f * __fmul_rn(__fsub_rn(qx[q], Cx), sig);
+                        const float by = -2.0f * __fmul_rn(__fsub_rn(qy[q], Cy), sig);
+                        h16.A[q] = __float2half2_rn(ax);
+                        h16.B[q] = __float2half2_rn(by);
+                        h16.T[q] = valid[q] ? h16_threshold(st.buf[q][K - 1], qx[q], qy[q], Cx, Cy, sig,
+                                                            h16.A[q], h16.B[q])
+                                            : -pos_inf<float>();
+                    }
+                }
+            }
+        }
         ring.release(t, ntiles, issue);
     }
     if constexpr (SPLIT)
@@ -478,9 +564,9 @@ template <typename T> static int knn_finish(const KnnArgs<T> &a, int S, cudaStre
 }
 
 // ---------------------------------------------------------------------------------
-template <typename T, int K, int Q, int G, int SPLIT, int MINB> static int set_filter_attrs(size_t smem)
+template <typename T, int K, int Q, int G, int SPLIT, int MINB, bool H16 = false> static int set_filter_attrs(size_t smem)
 {
-    auto kern = knn_filter_kernel<T, K, Q, G, SPLIT, MINB>;
+    auto kern = knn_filter_kernel<T, K, Q, G, SPLIT, MINB, H16>;
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
                    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) == cudaSuccess
                ? 0
@@ -508,7 +594,17 @@ static bool seed_unordered()
     return !(e && e[0] == '0');
 }
 
-template <int K, int Q, int G = 8, int MINB = 0, typename T = float>
+// H16 (fp32, spatially ordered batches only): the fp16 pre-filter kernels; AIDW_KNN_H16=0
+// turns them off (tests compare both).
+static int knn_h16_mode()
+{
+    const char *e = getenv("AIDW_KNN_H16");
+    // 0 off, 1 register-capped (128 registers, 4 CTAs/SM; C4 kNN 85.9 ms), 2 uncapped
+    // (168 registers, 3 CTAs/SM; 90.4 ms) -- profiles/r02_tune_knn_h16.log
+    return e ? atoi(e) : 1;
+}
+
+template <int K, int Q, int G = 8, int MINB = 0, typename T = float, bool H16 = false>
 static int launch_knn_filter_t(KnnArgs<T> a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp,
                                FilterData *fd)
 {
@@ -521,8 +617,8 @@ static int launch_knn_filter_t(KnnArgs<T> a, const FilterArgs &f, cudaStream_t s
     // factor that best fills the last wave (ordered_split_factor); an unordered one by
     // whole extra waves (knn_split_factor: its splits restart the top-k warm-up).
     const bool ordered = fd && fd->cell_start && order_queries(a.nq);
-    if (ordered && set_filter_attrs<T, K, Q, G, 1, MINB>(smem) < 0) return -1;
-    const int S = ordered ? ordered_split_factor((const void *)knn_filter_kernel<T, K, Q, G, 1, MINB>, smem,
+    if (ordered && set_filter_attrs<T, K, Q, G, 1, MINB, H16>(smem) < 0) return -1;
+    const int S = ordered ? ordered_split_factor((const void *)knn_filter_kernel<T, K, Q, G, 1, MINB, H16>, smem,
                                                  grid, (int)(a.ndp / kTileKF), a, sp)
                           : knn_split_factor((const void *)knn_filter_kernel<T, K, Q, G, 0, MINB>, smem, grid,
                                              (int)(a.ndp / kTileKF), a, sp);
@@ -545,7 +641,12 @@ static int launch_knn_filter_t(KnnArgs<T> a, const FilterArgs &f, cudaStream_t s
         }
     }
     if (S == 1) {
-        knn_filter_kernel<T, K, Q, G, 0, MINB><<<grid, kBlock, smem, st>>>(a, fo);
+        if (H16 && ordered) {
+            if (set_filter_attrs<T, K, Q, G, 0, MINB, H16>(smem) < 0) return -1;
+            knn_filter_kernel<T, K, Q, G, 0, MINB, H16><<<grid, kBlock, smem, st>>>(a, fo);
+        } else {
+            knn_filter_kernel<T, K, Q, G, 0, MINB><<<grid, kBlock, smem, st>>>(a, fo);
+        }
     } else {
         if (!ordered && fd && fd->cell_start && seed_unordered()) {  // per-query seed (§4.6)
             const float *c = static_cast<const float *>(fd->arrays);
@@ -558,8 +659,8 @@ static int launch_knn_filter_t(KnnArgs<T> a, const FilterArgs &f, cudaStream_t s
             }
         }
         if (ordered) {
-            if (set_filter_attrs<T, K, Q, G, 1, MINB>(smem) < 0) return -1;
-            knn_filter_kernel<T, K, Q, G, 1, MINB><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, fo);
+            if (set_filter_attrs<T, K, Q, G, 1, MINB, H16>(smem) < 0) return -1;
+            knn_filter_kernel<T, K, Q, G, 1, MINB, H16><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, fo);
         } else {
             if (set_filter_attrs<T, K, Q, G, 2, MINB>(smem) < 0) return -1;
             knn_filter_kernel<T, K, Q, G, 2, MINB><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, fo);
@@ -626,7 +727,14 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
     if (k <= 4) return launch_knn_filter_t<4, 2, 16>(a, f, st, sp, fd);
     if (k <= 8) return launch_knn_filter_t<8, 2, 16>(a, f, st, sp, fd);
     if (k <= 10) {  // large (spatially ordered) batches: Q = 4, G = 32 (108 vs 115 ms at C4)
-        if (order_queries(a.nq) && a.nq >= 32768) return launch_knn_filter_t<10, 4, 32>(a, f, st, sp, fd);
+        if (order_queries(a.nq) && a.nq >= 32768) {
+            switch (knn_h16_mode()) {
+            case 1: return launch_knn_filter_t<10, 4, 32, 4, float, true>(a, f, st, sp, fd);
+            case 2: return launch_knn_filter_t<10, 4, 32, 0, float, true>(a, f, st, sp, fd);
+            default: break;
+            }
+            return launch_knn_filter_t<10, 4, 32>(a, f, st, sp, fd);
+        }
         return launch_knn_filter_t<10, 2, 16>(a, f, st, sp, fd);
     }
     if (k <= 12) return launch_knn_filter_t<12, 2, 16>(a, f, st, sp, fd);

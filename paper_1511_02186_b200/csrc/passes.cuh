@@ -9,6 +9,8 @@
 #include "packed.cuh"
 #include "f64_tables.h"
 
+#include <cuda_fp16.h>
+
 namespace aidw {
 
 // ------------------------------------------------------------------ tile ring
@@ -217,6 +219,59 @@ __device__ __forceinline__ void filter8(const KnnF32State<K, Q, T> &st, int q, c
     }
 }
 
+// Rare path of a G-point group: for every query some lane's filter
+// flagged (hq), re-derive the group's fp32 filter values, build the bitmask of pairs that
+// pass the exact-safe fp32 threshold and re-check only those with the CANONICAL distance
+// on the original coordinates; the insertion is decided on that value.  One threshold
+// update per group (all of the group's candidates were checked against the current k-th
+// distance).  `on_thr` is called with the query slot after its threshold changed.
+template <int K, int Q, int G, typename T, class OnThr>
+__device__ __forceinline__ void knn_rare_group_impl(KnnF32State<K, Q, T> &st, const bool (&hq)[Q],
+                                                    const float *__restrict__ tcx, const float *__restrict__ tcy,
+                                                    const float *__restrict__ tpp, const T *__restrict__ tpx,
+                                                    const T *__restrict__ tpy, int j, OnThr &&on_thr)
+{
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        if (!__any_sync(0xffffffffu, hq[q])) continue;
+        unsigned mask = 0;
+        if (hq[q]) {
+#pragma unroll
+            for (int c = 0; c < G; c += 8) {
+                float t[8];
+                filter8(st, q, tcx, tcy, tpp, j + c, t);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) mask |= (t[e] <= st.thr[q]) ? (1u << (c + e)) : 0u;
+            }
+        }
+        bool inserted = false;
+        while (__any_sync(0xffffffffu, mask != 0)) {
+            if (mask) {
+                const int e = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const T s = dist_sq(st.qx[q], st.qy[q], tpx[j + e], tpy[j + e]);
+                if (s < st.buf[q][K - 1]) {
+                    topk_insert<T, K>(st.buf[q], s);
+                    inserted = true;
+                }
+            }
+        }
+        if (inserted) {
+            st.thr[q] = thr_of(thr_f32(st.buf[q][K - 1]), st.qqf[q], st.mf[q], st.Ef[q]);
+            on_thr(q);
+        }
+    }
+}
+
+template <int K, int Q, int G, typename T>
+__device__ __forceinline__ void knn_rare_group(KnnF32State<K, Q, T> &st, const bool (&hq)[Q],
+                                               const float *__restrict__ tcx, const float *__restrict__ tcy,
+                                               const float *__restrict__ tpp, const T *__restrict__ tpx,
+                                               const T *__restrict__ tpy, int j)
+{
+    knn_rare_group_impl<K, Q, G>(st, hq, tcx, tcy, tpp, tpx, tpy, j, [](int) {});
+}
+
 // One smem tile of TILE points in groups of G points per warp vote.  The main loop keeps
 // only a running 3-input-min per query (chunks of 8 points: 8 FFMA2 + 4 FMNMX3 per query,
 // the smem loads shared by the Q queries); a group that passes for some lane re-derives
@@ -269,37 +324,120 @@ __device__ __forceinline__ void knn_f32_tile(KnnF32State<K, Q, T> &st, const flo
             hq[q] = mn[q] <= st.thr[q];
             hit |= hq[q];
         }
-        if (__any_sync(0xffffffffu, hit)) {
+        if (__any_sync(0xffffffffu, hit)) knn_rare_group<K, Q, G>(st, hq, tcx, tcy, tpp, tpx, tpy, j);
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// fp16 pre-filter of the fp32 kNN (round 2).  The CTA's queries are
+// spatial neighbours (Morton order, §4.7); with C their bbox centre and sigma a power of
+// two, every data point of a tile is converted ONCE per CTA to fp16 û = fl16(sigma (x - C_x)),
+// v̂ likewise, p̂p = fl16(û² + v̂²), and the main loop evaluates t̂ = p̂p + Â û + B̂ v̂ on
+// HFMA2 (two points per instruction) with a packed HMNMX2 min tree -- 25 % more pairs per
+// clock than the FFMA2 + FMNMX3 loop (tools/knn_loop_bench.cu).  A group flagged by the
+// fp16 test goes to the SAME rare path as before (exact-safe fp32 filter, then the
+// canonical re-check), so the fp16 stage only has to keep every true candidate: its
+// threshold T (h16_threshold) is the k-th canonical distance on the t scale plus a
+// rigorous bound of every rounding (coordinates, p̂p, the two fp16 FMAs, subnormals).
+// Conversions clamp |û|, |v̂| <= 256 and p̂p <= 32768; sigma keeps |q̃| and the candidates'
+// radius r within 16, so no candidate is clamped or overflows, and clamped far points
+// land at t̂ >= 16384, far above T.
+template <int Q> struct KnnH16 {
+    __half2 A[Q], B[Q];  // splats of fl16(-2 sigma (q - C))
+    float T[Q];          // fp16-stage threshold (t scale, fp32, rounded up); -inf for empty slots
+};
+
+constexpr float kH16Clamp = 256.0f, kH16PPClamp = 32768.0f, kH16Radius = 16.0f;
+
+// T for a canonical k-th distance v (DESIGN.md §4.1 "fp16 pre-filter margin"): a true
+// candidate has s_canon < v, so sigma² s_exact <= r², r = sigma sqrt(v (1 + 2^-20)); with
+// Q = sigma |q - C|, p = q + d (|d| <= r): |p̃| <= P = Q + r, the rounded coordinates move
+// the pair by Delta <= up (2Q + r), |first FMA| <= (P + Delta)², |t̂| <= Q² + (r + Delta)²,
+// and t̂ <= (r + Delta)² - |q̂|² + up (P + Delta)² + 1.002 u16 ((P + Delta)² + Q² + (r + Delta)²)
+// + 2^-18 (absolute slack: fp16 subnormal coordinates and results, <= 2^-25 each; sigma
+// keeps the candidates' scaled magnitudes O(1..32), so this is far below T).  |q̂|² is exact
+// from the fp16 coefficients.
+__device__ __forceinline__ float h16_threshold(float v, float qx, float qy, float Cx, float Cy, float sig,
+                                               __half2 A, __half2 B)
+{
+    if (!(v < pos_inf<float>())) return pos_inf<float>();
+    const double u16 = 0x1p-11, up = 0x1p-11 + 0x1p-22;
+    const double dx = (double)qx - (double)Cx, dy = (double)qy - (double)Cy;
+    const double Qn = (double)sig * sqrt(dx * dx + dy * dy) * (1.0 + 0x1p-40);
+    const double r = (double)sig * sqrt((double)v * (1.0 + 0x1p-20));
+    const double ah = 0.5 * (double)__low2float(A), bh = 0.5 * (double)__low2float(B);
+    const double qq = ah * ah + bh * bh;  // |q̂|², exact
+    const double Qb = fmax(Qn, sqrt(qq)) * (1.0 + up);
+    const double D = up * (2.0 * Qb + r);
+    const double P = Qb + r + D, R = r + D;
+    const double T = R * R - qq + up * P * P + 1.002 * u16 * (P * P + Qb * Qb + R * R) + 0x1p-18;
+    return __double2float_ru(T);
+}
+
+// One tile's fp16 copy: TILE/2 couples of (û, v̂, p̂p), all threads of the CTA.
+template <int TILE>
+__device__ __forceinline__ void h16_convert(const float *__restrict__ tpx, const float *__restrict__ tpy,
+                                            __half2 *__restrict__ hu, __half2 *__restrict__ hv,
+                                            __half2 *__restrict__ hp, float Cx, float Cy, float sig)
+{
+    for (int i = threadIdx.x; i < TILE / 2; i += blockDim.x) {
+        const float2 x = *reinterpret_cast<const float2 *>(tpx + 2 * i);
+        const float2 y = *reinterpret_cast<const float2 *>(tpy + 2 * i);
+        const float u0 = fminf(fmaxf(__fmul_rn(__fsub_rn(x.x, Cx), sig), -kH16Clamp), kH16Clamp);
+        const float u1 = fminf(fmaxf(__fmul_rn(__fsub_rn(x.y, Cx), sig), -kH16Clamp), kH16Clamp);
+        const float v0 = fminf(fmaxf(__fmul_rn(__fsub_rn(y.x, Cy), sig), -kH16Clamp), kH16Clamp);
+        const float v1 = fminf(fmaxf(__fmul_rn(__fsub_rn(y.y, Cy), sig), -kH16Clamp), kH16Clamp);
+        const __half2 U = __floats2half2_rn(u0, u1), V = __floats2half2_rn(v0, v1);
+        const float2 uf = __half22float2(U), vf = __half22float2(V);
+        const float p0 = fminf(__fmaf_rn(uf.x, uf.x, __fmul_rn(vf.x, vf.x)), kH16PPClamp);
+        const float p1 = fminf(__fmaf_rn(uf.y, uf.y, __fmul_rn(vf.y, vf.y)), kH16PPClamp);
+        hu[i] = U;
+        hv[i] = V;
+        hp[i] = __floats2half2_rn(p0, p1);
+    }
+}
+
+// The fp16 main loop over one tile (same groups, votes and rare path as knn_f32_tile).
+template <int K, int Q, int G, int TILE>
+__device__ __forceinline__ void knn_h16_tile(KnnF32State<K, Q, float> &st, KnnH16<Q> &h, const __half2 *hu,
+                                             const __half2 *hv, const __half2 *hp, const float *__restrict__ tcx,
+                                             const float *__restrict__ tcy, const float *__restrict__ tpp,
+                                             const float *__restrict__ tpx, const float *__restrict__ tpy,
+                                             float Cx, float Cy, float sig)
+{
+    static_assert(G % 8 == 0 && G <= 32 && TILE % G == 0, "group size");
+    const uint32_t au = smem_addr(hu), av = smem_addr(hv), ap = smem_addr(hp);
+#pragma unroll 1
+    for (int j = 0; j < TILE; j += G) {
+        __half2 mn[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) mn[q] = __half2half2(__ushort_as_half((unsigned short)0x7c00));  // +inf
+#pragma unroll
+        for (int c = 0; c < G; c += 8) {
+            const uint32_t o = (uint32_t)(j + c) * 2u;  // 8 points = 4 half2 = 16 bytes
+            const float4 U4 = lds128(au + o), V4 = lds128(av + o), P4 = lds128(ap + o);
+            const __half2 *u = reinterpret_cast<const __half2 *>(&U4);
+            const __half2 *v = reinterpret_cast<const __half2 *>(&V4);
+            const __half2 *pp = reinterpret_cast<const __half2 *>(&P4);
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
-                if (!__any_sync(0xffffffffu, hq[q])) continue;
-                unsigned mask = 0;
-                if (hq[q]) {
+                __half2 t[4];
 #pragma unroll
-                    for (int c = 0; c < G; c += 8) {
-                        float t[8];
-                        filter8(st, q, tcx, tcy, tpp, j + c, t);
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) mask |= (t[e] <= st.thr[q]) ? (1u << (c + e)) : 0u;
-                    }
-                }
-                bool inserted = false;
-                while (__any_sync(0xffffffffu, mask != 0)) {
-                    if (mask) {
-                        const int e = __ffs(mask) - 1;
-                        mask &= mask - 1;
-                        const T s = dist_sq(st.qx[q], st.qy[q], tpx[j + e], tpy[j + e]);
-                        if (s < st.buf[q][K - 1]) {
-                            topk_insert<T, K>(st.buf[q], s);
-                            inserted = true;
-                        }
-                    }
-                }
-                // one threshold update per group (candidates of this group were all
-                // checked exactly against the current k-th distance above)
-                if (inserted) st.thr[q] = thr_of(thr_f32(st.buf[q][K - 1]), st.qqf[q], st.mf[q], st.Ef[q]);
+                for (int e = 0; e < 4; ++e) t[e] = __hfma2(h.B[q], v[e], __hfma2(h.A[q], u[e], pp[e]));
+                mn[q] = __hmin2(__hmin2(__hmin2(t[0], t[1]), __hmin2(t[2], t[3])), mn[q]);
             }
         }
+        bool hq[Q], hit = false;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const float2 m = __half22float2(mn[q]);
+            hq[q] = fminf(m.x, m.y) <= h.T[q];
+            hit |= hq[q];
+        }
+        if (__any_sync(0xffffffffu, hit))
+            knn_rare_group_impl<K, Q, G>(st, hq, tcx, tcy, tpp, tpx, tpy, j, [&](int q) {
+                h.T[q] = h16_threshold(st.buf[q][K - 1], st.qx[q], st.qy[q], Cx, Cy, sig, h.A[q], h.B[q]);
+            });
     }
 }
 

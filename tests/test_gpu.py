@@ -233,6 +233,42 @@ def test_coincident_queries(P, orc, dtype):
     assert np.allclose(Zg[64:69], (z[:5] + z[5:10]) / 2, rtol=TOL[dtype])
 
 
+@pytest.mark.parametrize("case", ["uniform", "clustered", "offset", "tiny", "outliers"])
+@pytest.mark.parametrize("h16", ["1", "2"])
+def test_knn_h16_bit_identical(P, orc, monkeypatch, case, h16):
+    """The fp16 pre-filter of spatially ordered fp32 batches (passes.cuh knn_h16_tile; its
+    threshold carries a rigorous rounding margin) never drops a true candidate: lists,
+    r_obs, d1^2 and the bounds are bit-identical to the fp32-filter kernel
+    (AIDW_KNN_H16=0) and the lists bit-exact against the oracle on a sample -- uniform and
+    clustered data, coordinates offset by 1000 (fp32 ulp 6e-5) or scaled by 2^-30,
+    duplicated points, coincident queries and queries far outside the data."""
+    nq = 40000
+    if case == "clustered":
+        x, y, z = datagen.make_data({"nd": 50000, "data": "clustered"}, seed=77)
+        qx, qy = datagen.uniform_points(78, nq, datagen.S_QX, datagen.S_QY)
+    else:
+        x, y, z, qx, qy = datagen.random_cloud(91, 50000, nq)
+    if case in ("offset", "tiny"):
+        f = ((lambda v: (1000.0 + v).astype(np.float32).astype(np.float64)) if case == "offset" else
+             (lambda v: v * 2.0 ** -30))
+        x, y, qx, qy = f(x), f(y), f(qx), f(qy)
+    if case == "outliers":
+        x[1::7], y[1::7] = x[::7][: len(x[1::7])], y[::7][: len(y[1::7])]  # duplicates
+        qx[::13], qy[::13] = x[: len(qx[::13])], y[: len(qy[::13])]       # coincident
+        qx[::501] = qx[::501] * 50.0 - 20.0                               # far outside
+    res = {}
+    for flag in ("0", h16):
+        monkeypatch.setenv("AIDW_KNN_H16", flag)
+        eng = P.AIDW(x, y, z)
+        res[flag] = gpu_knn(P, eng, qx, qy, 10)
+        eng.close()
+    for u, v in zip(res["0"], res[h16]):
+        assert np.array_equal(u, v)
+    sub = np.arange(0, nq, 211)
+    ro, do = orc.knn_f32(x, y, qx[sub], qy[sub], 10, want_dists=True)
+    assert np.array_equal(res[h16][3][sub], do) and np.array_equal(res[h16][0][sub], ro)
+
+
 @pytest.mark.parametrize("nd,nq", [(3000, 777), (100003, 20000), (262144, 65536)])
 def test_exp2_clamp_free_bit_identical(P, monkeypatch, nd, nq):
     """The fp32 weighting pass drops the polynomial exp2's clamp on tiles without padding

@@ -9,6 +9,7 @@
 // Prints one JSON line per variant: pairs per clock per SM and the FMA-pipe fraction
 // (1 FFMA2 = 2 FMA lanes per pair; 128 FMA lanes/clk/SM).
 #include <cstdio>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 constexpr int TILE = 512;
@@ -166,10 +167,71 @@ __global__ void __launch_bounds__(THREADS) knn_loop_uni(const float *__restrict_
     if (blockIdx.x == 0 && threadIdx.x == 0) *clk = Clk{c0, c1};
 }
 
+// VAR 7 (separate kernel): the product loop's layout (lanes = queries, broadcast smem
+// points) in fp16: t = pp + A cx + B cy on HFMA2 (2 points per instruction), a packed
+// HMNMX2 min tree, 8-point chunks.  Tests whether the half2 pipes beat FFMA2 + FMNMX3.
+template <int Q, int G, int VAR>
+__global__ void __launch_bounds__(THREADS) knn_loop_h2(const float *__restrict__ g, float *out, int reps, Clk *clk)
+{
+    extern __shared__ __align__(16) float sm[];
+    __half2 *hx = reinterpret_cast<__half2 *>(sm);  // TILE/2 couples each
+    __half2 *hy = hx + TILE / 2, *hp = hy + TILE / 2;
+    for (int i = threadIdx.x; i < TILE / 2; i += THREADS) {
+        hx[i] = __floats2half2_rn(g[2 * i], g[2 * i + 1]);
+        hy[i] = __floats2half2_rn(g[TILE + 2 * i], g[TILE + 2 * i + 1]);
+        hp[i] = __floats2half2_rn(g[2 * TILE + 2 * i], g[2 * TILE + 2 * i + 1]);
+    }
+    __syncthreads();
+    __half2 A[Q], B[Q];
+    float thr[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        A[q] = __float2half2_rn(opaque(-2.0f * (0.1f + 0.01f * q + 1e-6f * threadIdx.x)));
+        B[q] = __float2half2_rn(opaque(-2.0f * (0.3f - 0.01f * q)));
+        thr[q] = opaque(-1e30f);
+    }
+    float acc = 0.f;
+    unsigned long long c0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll 1
+        for (int j = 0; j < TILE / 2; j += G / 2) {
+            __half2 mn[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) mn[q] = __float2half2_rn(60000.f);
+#pragma unroll
+            for (int c = 0; c < G / 2; c += 4) {  // 8 points = 4 couples
+                const uint4 X = *reinterpret_cast<const uint4 *>(hx + j + c);
+                const uint4 Y = *reinterpret_cast<const uint4 *>(hy + j + c);
+                const uint4 P = *reinterpret_cast<const uint4 *>(hp + j + c);
+                const __half2 *xv = reinterpret_cast<const __half2 *>(&X);
+                const __half2 *yv = reinterpret_cast<const __half2 *>(&Y);
+                const __half2 *pv = reinterpret_cast<const __half2 *>(&P);
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    __half2 t[4];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) t[h] = __hfma2(B[q], yv[h], __hfma2(A[q], xv[h], pv[h]));
+                    mn[q] = __hmin2(__hmin2(__hmin2(t[0], t[1]), __hmin2(t[2], t[3])), mn[q]);
+                }
+            }
+            bool hit = false;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const float2 m = __half22float2(mn[q]);
+                hit |= fminf(m.x, m.y) <= thr[q];
+            }
+            if (__any_sync(0xffffffffu, hit)) acc += 1.f;
+        }
+    }
+    unsigned long long c1 = clock64();
+    if (acc == 1234.5f) out[0] = acc;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *clk = Clk{c0, c1};
+}
+
 template <int Q, int G, int VAR>
 static void run(const char *name, int ctas_per_sm, const float *g, float *out, Clk *clk, int sms, double mhz_ref)
 {
-    auto k = VAR == 6 ? knn_loop_uni<Q, G, VAR> : knn_loop<Q, G, VAR>;
+    auto k = VAR == 7 ? knn_loop_h2<Q, G, VAR> : VAR == 6 ? knn_loop_uni<Q, G, VAR> : knn_loop<Q, G, VAR>;
     // pad the dynamic smem so at most ctas_per_sm CTAs fit on an SM
     size_t smem = 3 * TILE * sizeof(float);
     const size_t per = (227 * 1024) / ctas_per_sm;
@@ -230,6 +292,8 @@ int main()
         run<8, 32, 6>("uniform_queries_q8", c, g, out, clk, sms, mhz);
         run<16, 32, 6>("uniform_queries_q16", c, g, out, clk, sms, mhz);
         run<32, 32, 6>("uniform_queries_q32", c, g, out, clk, sms, mhz);
+        run<4, 32, 7>("fp16_hfma2_hmin2_q4", c, g, out, clk, sms, mhz);
+        run<8, 32, 7>("fp16_hfma2_hmin2_q8", c, g, out, clk, sms, mhz);
     }
     return 0;
 }
