@@ -66,11 +66,11 @@ FMA_PER_CLK_SM = 123.2    # measured FFMA2 (packed) FMA ops per SM per clock
 KNN_FP32_PER_PAIR = 4     # canonical kNN distance (2 sub, mul, fma) -- SIMT FP32 bound
 N_SM = 148
 # fp64 (--dtype f64): the weighting pass has no hardware transcendental;
-# per pair it issues 25 FP64 instructions (distance 4, table + degree-5 log2 ~9, exponent
-# 1, table + degree-5 exp2 ~9, sums 2; counted on the ncu source page,
-# profiles/r01_ncu_interp_f64_v12.json) on the FP64 pipe; DFMA rate measured by
-# tools/pipe_peaks.cu (profiles/r01_pipe_peaks.json).
-DP_PER_PAIR = 25
+# per pair the kernel issues 21 FP64 operations (round 2: distance 4, table + degree-3
+# log2 6, exponent 1, table + degree-4 exp2 8, sums 2; round 1 issued 25 with degree-5
+# polynomials, profiles/archive_r01/r01_ncu_interp_f64_v12.json) on the FP64 pipe; DFMA rate
+# measured by tools/pipe_peaks.cu (profiles/r01_pipe_peaks.json).
+DP_PER_PAIR = 21
 DFMA_PER_CLK_SM = 63.23  # measured (profiles/r01_pipe_peaks.json dfma_per_clk_sm)
 # The algorithmic fp64 bound: FP64 ops per pair that evaluate Eq. 1 to
 # the north star's fp64 tolerance (1e-10 relative) -- distance 4, log2 with a 256-entry

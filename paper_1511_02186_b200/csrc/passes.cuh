@@ -446,10 +446,11 @@ __device__ __forceinline__ void knn_h16_tile(KnnF32State<K, Q, float> &st, KnnH1
 // libdevice's cost (~90 FP64 ops per pair for log2 + exp2).  Both use a small table in
 // shared memory (tools/gen_f64_tables.py) and a short Taylor polynomial:
 //  log2(s) = e + LOGM[i] + log2(1 + t),  t = m * C[i] - 1, i = top 8 mantissa bits,
-//            |t| <= 2^-9, degree 5 (truncation 1.3e-17); valid for normal s > 0.
-//  exp2(x) = 2^j * T[k] * 2^r,  64x = 64j + k + 64r rounded, |r| <= 1/128, degree 5
-//            (truncation < 4e-17); x clamped to >= -1000 (smaller weights vanish).
-// (v11: 256/64-entry tables instead of 64/16 save 4 of ~29 FP64 ops per pair.)
+//            |t| <= 2^-9, degree kLog2Deg = 3 (truncation 5.2e-12); valid for normal s > 0.
+//  exp2(x) = 2^j * T[k] * 2^r,  64x = 64j + k + 64r rounded, |r| <= 1/128, degree
+//            kExp2Deg = 4 (truncation 3.8e-14); x clamped to >= -1000 (smaller weights vanish).
+// (v11: 256/64-entry tables instead of 64/16 save 4 of ~29 FP64 ops per pair; round 2:
+// the tolerance-driven degrees of DESIGN.md §4.9 save 3 more -- 21 FP64 ops per pair.)
 __device__ __forceinline__ double log2_f64(double s, const double2 *__restrict__ tab)
 {
     const unsigned long long bits = (unsigned long long)__double_as_longlong(s);
@@ -458,9 +459,9 @@ __device__ __forceinline__ double log2_f64(double s, const double2 *__restrict__
     const double m = __longlong_as_double((long long)((bits & 0x000fffffffffffffull) | 0x3ff0000000000000ull));
     const double2 ci = tab[i];
     const double t = fma(m, ci.x, -1.0);
-    double p = kLog2Poly[4];
+    double p = kLog2Poly[kLog2Deg - 1];
 #pragma unroll
-    for (int k = 3; k >= 0; --k) p = fma(p, t, kLog2Poly[k]);
+    for (int k = kLog2Deg - 2; k >= 0; --k) p = fma(p, t, kLog2Poly[k]);
     // exponent as double without a conversion: 2^52 + be, minus (2^52 + 1023)
     const double ed = __longlong_as_double((long long)(0x4330000000000000ull | be)) - (4503599627370496.0 + 1023.0);
     return ed + fma(p, t, ci.y);
@@ -475,9 +476,9 @@ __device__ __forceinline__ double exp2_f64(double x, const double *__restrict__ 
     const double nd = t - kM;
     const double r = fma(nd, -1.0 / kN, x);
     const int n = (int)(unsigned)(unsigned long long)__double_as_longlong(t);
-    double p = kExp2Poly[5];
+    double p = kExp2Poly[kExp2Deg];
 #pragma unroll
-    for (int k = 4; k >= 0; --k) p = fma(p, r, kExp2Poly[k]);
+    for (int k = kExp2Deg - 1; k >= 0; --k) p = fma(p, r, kExp2Poly[k]);
     const double y = tab[n & ((1 << kExp2TabBits) - 1)] * p;
     // multiply by 2^(n >> bits) through the exponent field (no overflow: y <= 2, n <= 0)
     return __longlong_as_double(__double_as_longlong(y) + ((long long)(n >> kExp2TabBits) << 52));

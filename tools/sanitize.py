@@ -44,7 +44,16 @@ for dt in (torch.float32, torch.float64):
     eng.run_fixed(bx, by, 10)
     os.environ["AIDW_SPLIT"] = "0"
     eng.run(qx, qy, 10, LV, P.GLOBAL)
+    eng.run(bx, by, 10, LV, P.GLOBAL)  # unsplit ordered batch (fp16 pre-filter from tile 1)
     del os.environ["AIDW_SPLIT"]
+    os.environ["AIDW_KNN_H16"] = "2"  # the uncapped fp16 pre-filter kernel
+    eng.run(bx, by, 10, LV, P.GLOBAL)
+    del os.environ["AIDW_KNN_H16"]
+    # device-side bounds exchange with one rank (push, wait, acks)
+    eng.exchange_connect([eng.exchange_setup(0, 1)])
+    for _ in range(3):
+        eng.run(qx, qy, 10, LV, P.GLOBAL)
+    eng.exchange_close()
     torch.cuda.synchronize()
     eng.check()
 print("sanitize run ok")
