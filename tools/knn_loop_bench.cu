@@ -211,7 +211,15 @@ __global__ void __launch_bounds__(THREADS) knn_loop_h2(const float *__restrict__
                     __half2 t[4];
 #pragma unroll
                     for (int h = 0; h < 4; ++h) t[h] = __hfma2(B[q], yv[h], __hfma2(A[q], xv[h], pv[h]));
-                    mn[q] = __hmin2(__hmin2(__hmin2(t[0], t[1]), __hmin2(t[2], t[3])), mn[q]);
+                    if (VAR == 8) {  // HFMA2 only: fold t into the running value with one more HFMA2
+                        mn[q] = __hfma2(t[0], t[1], __hfma2(t[2], t[3], mn[q]));
+                    } else if (VAR == 9) {  // compare per couple against the threshold (HSETP2) instead of a min tree
+                        const __half2 th = __float2half2_rn(thr[q]);
+                        const bool hh = __hble2(t[0], th) | __hble2(t[1], th) | __hble2(t[2], th) | __hble2(t[3], th);
+                        if (hh) mn[q] = __float2half2_rn(-1.0f);
+                    } else {
+                        mn[q] = __hmin2(__hmin2(__hmin2(t[0], t[1]), __hmin2(t[2], t[3])), mn[q]);
+                    }
                 }
             }
             bool hit = false;
@@ -231,7 +239,7 @@ __global__ void __launch_bounds__(THREADS) knn_loop_h2(const float *__restrict__
 template <int Q, int G, int VAR>
 static void run(const char *name, int ctas_per_sm, const float *g, float *out, Clk *clk, int sms, double mhz_ref)
 {
-    auto k = VAR == 7 ? knn_loop_h2<Q, G, VAR> : VAR == 6 ? knn_loop_uni<Q, G, VAR> : knn_loop<Q, G, VAR>;
+    auto k = (VAR >= 7) ? knn_loop_h2<Q, G, VAR> : VAR == 6 ? knn_loop_uni<Q, G, VAR> : knn_loop<Q, G, VAR>;
     // pad the dynamic smem so at most ctas_per_sm CTAs fit on an SM
     size_t smem = 3 * TILE * sizeof(float);
     const size_t per = (227 * 1024) / ctas_per_sm;
@@ -294,6 +302,8 @@ int main()
         run<32, 32, 6>("uniform_queries_q32", c, g, out, clk, sms, mhz);
         run<4, 32, 7>("fp16_hfma2_hmin2_q4", c, g, out, clk, sms, mhz);
         run<8, 32, 7>("fp16_hfma2_hmin2_q8", c, g, out, clk, sms, mhz);
+        run<4, 32, 8>("fp16_hfma2_only_q4", c, g, out, clk, sms, mhz);
+        run<4, 32, 9>("fp16_hfma2_hsetp2_q4", c, g, out, clk, sms, mhz);
     }
     return 0;
 }
