@@ -745,10 +745,18 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
         case 18: return launch_knn_filter_t<15, 1, 32>(a, f, st, sp, fd);
         case 19: return launch_knn_filter_t<15, 2, 8>(a, f, st, sp, fd);
         case 20: return launch_knn_filter_t<15, 1, 16>(a, f, st, sp, fd);
+        case 21: return launch_knn_filter_t<15, 2, 32, 0, float, true>(a, f, st, sp, fd);  // fp16 pre-filter
+        case 22: return launch_knn_filter_t<15, 4, 32, 4, float, true>(a, f, st, sp, fd);
+        case 23: return launch_knn_filter_t<15, 2, 32, 6, float, true>(a, f, st, sp, fd);
         default: break;
         }
     }
-    if (k <= 15) return launch_knn_filter_t<15, 2, 32>(a, f, st, sp, fd);  // C3: 1.95 vs 2.03 ms (G = 16)
+    if (k <= 15) {  // C3: 1.95 vs 2.03 ms (G = 16); ordered batches with the fp16 pre-filter
+                    // (Q = 2, uncapped): C3 kNN 1.82 -> 1.59 ms (profiles/r02_tune_knn_c3_h16.log)
+        if (order_queries(a.nq) && a.nq >= 32768 && knn_h16_mode() != 0)
+            return launch_knn_filter_t<15, 2, 32, 0, float, true>(a, f, st, sp, fd);
+        return launch_knn_filter_t<15, 2, 32>(a, f, st, sp, fd);
+    }
     if (k <= 16) return launch_knn_filter_t<16, 2, 16>(a, f, st, sp, fd);
     if (k <= 24) return launch_knn_filter_t<24, 2>(a, f, st, sp, fd);
     return launch_knn_filter_t<32, 2>(a, f, st, sp, fd);

@@ -233,9 +233,10 @@ def test_coincident_queries(P, orc, dtype):
     assert np.allclose(Zg[64:69], (z[:5] + z[5:10]) / 2, rtol=TOL[dtype])
 
 
-@pytest.mark.parametrize("case", ["uniform", "clustered", "offset", "tiny", "outliers"])
+@pytest.mark.parametrize("case,k", [("uniform", 10), ("clustered", 10), ("offset", 10), ("tiny", 10),
+                                    ("outliers", 10), ("clustered", 15), ("outliers", 15)])
 @pytest.mark.parametrize("h16", ["1", "2"])
-def test_knn_h16_bit_identical(P, orc, monkeypatch, case, h16):
+def test_knn_h16_bit_identical(P, orc, monkeypatch, case, k, h16):
     """The fp16 pre-filter of spatially ordered fp32 batches (passes.cuh knn_h16_tile; its
     threshold carries a rigorous rounding margin) never drops a true candidate: lists,
     r_obs, d1^2 and the bounds are bit-identical to the fp32-filter kernel
@@ -260,12 +261,12 @@ def test_knn_h16_bit_identical(P, orc, monkeypatch, case, h16):
     for flag in ("0", h16):
         monkeypatch.setenv("AIDW_KNN_H16", flag)
         eng = P.AIDW(x, y, z)
-        res[flag] = gpu_knn(P, eng, qx, qy, 10)
+        res[flag] = gpu_knn(P, eng, qx, qy, k)
         eng.close()
     for u, v in zip(res["0"], res[h16]):
         assert np.array_equal(u, v)
     sub = np.arange(0, nq, 211)
-    ro, do = orc.knn_f32(x, y, qx[sub], qy[sub], 10, want_dists=True)
+    ro, do = orc.knn_f32(x, y, qx[sub], qy[sub], k, want_dists=True)
     assert np.array_equal(res[h16][3][sub], do) and np.array_equal(res[h16][0][sub], ro)
 
 
