@@ -718,6 +718,10 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
         case 13: return launch_knn_filter_t<10, 2, 32, 8>(a, f, st, sp, fd);
         case 14: return launch_knn_filter_t<10, 1, 16>(a, f, st, sp, fd);
         case 15: return launch_knn_filter_t<10, 1, 32>(a, f, st, sp, fd);
+        case 24: return launch_knn_filter_t<10, 4, 16, 4, float, true>(a, f, st, sp, fd);  // fp16, G = 16
+        case 25: return launch_knn_filter_t<10, 2, 32, 0, float, true>(a, f, st, sp, fd);  // fp16, Q = 2
+        case 26: return launch_knn_filter_t<10, 2, 32, 6, float, true>(a, f, st, sp, fd);  // fp16, Q = 2, 6 CTAs/SM
+        case 27: return launch_knn_filter_t<10, 3, 32, 5, float, true>(a, f, st, sp, fd);  // fp16, Q = 3
         default: break;
         }
     }
@@ -729,7 +733,11 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
     if (k <= 10) {  // large (spatially ordered) batches: Q = 4, G = 32 (108 vs 115 ms at C4)
         if (order_queries(a.nq) && a.nq >= 32768) {
             switch (knn_h16_mode()) {
-            case 1: return launch_knn_filter_t<10, 4, 32, 4, float, true>(a, f, st, sp, fd);
+            case 1:  // Q = 2 (6 CTAs/SM) below ~384K queries (strong-scaled shares): 128,000
+                     // 13.8 -> 13.0 ms, 32,768 7.1 -> 6.1; Q = 4 above (C4 86.8 vs 89.2 ms)
+                     // -- profiles/r02_tune_knn_h16_q.log
+                if (a.nq < 393216) return launch_knn_filter_t<10, 2, 32, 6, float, true>(a, f, st, sp, fd);
+                return launch_knn_filter_t<10, 4, 32, 4, float, true>(a, f, st, sp, fd);
             case 2: return launch_knn_filter_t<10, 4, 32, 0, float, true>(a, f, st, sp, fd);
             default: break;
             }

@@ -243,7 +243,7 @@ def test_knn_h16_bit_identical(P, orc, monkeypatch, case, k, h16):
     (AIDW_KNN_H16=0) and the lists bit-exact against the oracle on a sample -- uniform and
     clustered data, coordinates offset by 1000 (fp32 ulp 6e-5) or scaled by 2^-30,
     duplicated points, coincident queries and queries far outside the data."""
-    nq = 40000
+    nq = 40000 if case != "uniform" else 400000  # mode 1: Q = 2 below 393,216 queries, Q = 4 above
     if case == "clustered":
         x, y, z = datagen.make_data({"nd": 50000, "data": "clustered"}, seed=77)
         qx, qy = datagen.uniform_points(78, nq, datagen.S_QX, datagen.S_QY)

@@ -1,7 +1,10 @@
-# GPU check (r02n): pytest -m gpu (k = 15 fp16 pre-filter), configs C3 timing
+# GPU check (r02q): kNN shape by batch size -- tests, strong shares, bench
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/${1:-r02n}
+O=gpurun_out/${1:-r02q}
 mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -q -rf -k "not C5" > $O/pytest_gpu.log 2>&1; echo rc=$? >> $O/pytest_gpu.log
-timeout 600 python tools/configs_bench.py --configs C2,C3 --out $O/configs_c3.json > $O/configs.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu.py -q -rf -k "h16 or golden and C4 or graph or order or seed or split" > $O/pytest.log 2>&1; echo rc=$? >> $O/pytest.log
+for nq in 512000 256000 128000; do
+  timeout 300 python bench.py --nq $nq --no-cpu-baseline --no-e2e --no-f64 > $O/strong_share_$nq.json 2>> $O/bench.err
+done
+timeout 900 python bench.py --no-cpu-baseline > $O/bench.json 2>> $O/bench.err
 echo done
