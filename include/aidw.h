@@ -33,8 +33,10 @@
  *    (DESIGN.md §4.6-4.7, §5).  The handle owns growable device scratch for the
  *    small-nq data split and the spatial query order (allocated on first use).
  *  - Tuning/testing environment variables (defaults are the measured best):
- *    AIDW_SPLIT=0|n (data split off / forced factor) and AIDW_KNN_ORDER=0 (no
- *    spatial query order) are read per call; AIDW_ALPHA_CLASSES=0 (no
+ *    AIDW_SPLIT=0|n (data split off / forced factor), AIDW_KNN_ORDER=0 (no
+ *    spatial query order), AIDW_KNN_H16=0|1|2 (fp16 kNN pre-filter off / default /
+ *    uncapped registers) and AIDW_EXP2_CLAMP=1 (always-clamped polynomial exp2) are read
+ *    per call -- none changes a result; AIDW_ALPHA_CLASSES=0 (no
  *    exact-exponent weighting classes) and AIDW_KNN_VARIANT / AIDW_INTERP_VARIANT
  *    (tuning sweeps) once per process; AIDW_KNN_FILTER=0 (canonical kNN, no fp32
  *    filter, for either dtype) at aidw_create.  Spatially ordered kNN batches
