@@ -1,0 +1,19 @@
+# Round-2 final evidence (run under gpurun from the repo root): bash tools/gpu_final_r02.sh TAG
+# build + smoke, pytest -m gpu (C4 + C5 golden), the default bench line, C5 strong N = 1,
+# a 2-rank gloo logic run of the default bench (ranks share the GPU), the reference
+# (oracle) arm, the ncu launch list of the bench step, the Table-1 ablation.
+cd "${GRAFT_REPO_ROOT:-.}"
+TAG=${1:-r02final}
+O=gpurun_out/$TAG
+mkdir -p $O
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $O/smoke.log 2>&1; echo rc=$? >> $O/smoke.log
+timeout 1800 python -m pytest tests -m gpu -q -rf > $O/pytest_gpu.log 2>&1; echo rc=$? >> $O/pytest_gpu.log
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
+timeout 900 python bench.py --config C5 --steps 3 --no-f64 --no-cpu-baseline > $O/bench_c5.json 2>> $O/bench.err
+AIDW_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+    --master-addr 127.0.0.1 --master-port 29541 bench.py --gpus 2 --steps 3 --warmup 3 > $O/bench_gloo2.json 2> $O/bench_gloo2.err
+timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > $O/bench_ref.json 2>> $O/bench.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
+    python bench.py --profile --warmup 1 > /dev/null 2>&1
+timeout 1200 python tools/table1.py --out $O/table1.md --json $O/table1.jsonl > $O/table1.log 2>&1
+echo done
