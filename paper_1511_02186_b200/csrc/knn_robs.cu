@@ -351,7 +351,10 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
         home = (int)(f.cell_start[morton_cell((float)a.qx[qm], (float)a.qy[qm], f.grid)] / TILE);
         home = home >= nt_all ? nt_all - 1 : home;
     }
-    const bool seed = SPLIT && a.perm != nullptr;
+    // H16 kernels seed every query's lists from its own Morton cell instead (per-query seed,
+    // f.sx != null): no home tile to scan, and the fp16 loop starts on the first tile
+    const bool qseed = H16 && a.perm != nullptr && f.sx != nullptr;
+    const bool seed = SPLIT && a.perm != nullptr && !qseed;
     int start = 0;
     if (!SPLIT && a.perm) start = home == 0 ? nt_all - 1 : home - 1;
     const int ntiles = tr.nloc + (seed ? 1 : 0);
@@ -394,6 +397,13 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
                 if (valid[q]) st.seed_query(q, f, a.k, k0);
         }
     }
+    if constexpr (H16) {  // ordered fp16 kernels: per-query seed
+        if (qseed) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (valid[q]) st.seed_query(q, f, a.k, k0);
+        }
+    }
 
     // fp16 pre-filter state (H16): the CTA's query-bbox centre, the scale, per-query
     // coefficients and thresholds; enabled once every query has a finite k-th distance
@@ -424,6 +434,45 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
         __syncthreads();  // hred is reused for the scale
     }
 
+    // fp16 pre-filter setup once every list is finite: the CTA scale sigma (sigma m <= 16, m
+    // the largest |q - C| and k-th distance over the CTA), per-query coefficients and
+    // thresholds.  All threads; the result is CTA-uniform.
+    auto h16_enable = [&]() -> bool {
+        bool fin = true;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) fin &= !valid[q] || st.buf[q][K - 1] < pos_inf<float>();
+        if (!__syncthreads_and(fin)) return false;
+        float m = 0.f;  // non-negative: float bits order like uint
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            if (valid[q]) {
+                const float dx = qx[q] - Cx, dy = qy[q] - Cy;
+                m = fmaxf(m, fmaxf(sqrtf(dx * dx + dy * dy), sqrtf((float)st.buf[q][K - 1])));
+            }
+        if (threadIdx.x == 0) hred[0] = 0u;
+        __syncthreads();
+        atomicMax(&hred[0], __float_as_uint(m * 1.001f));
+        __syncthreads();
+        const float mm = __uint_as_float(hred[0]);
+        int e = 0;
+        frexpf(kH16Radius / fmaxf(mm, 0x1p-100f), &e);  // 16/m = f 2^e, f in [0.5, 1)
+        e = e - 1 < -100 ? -100 : (e - 1 > 100 ? 100 : e - 1);
+        sig = ldexpf(1.0f, e);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const float ax = -2.0f * __fmul_rn(__fsub_rn(qx[q], Cx), sig);
+            const float by = -2.0f * __fmul_rn(__fsub_rn(qy[q], Cy), sig);
+            h16.A[q] = __float2half2_rn(ax);
+            h16.B[q] = __float2half2_rn(by);
+            h16.T[q] = valid[q] ? h16_threshold(st.buf[q][K - 1], qx[q], qy[q], Cx, Cy, sig, h16.A[q], h16.B[q])
+                                : -pos_inf<float>();
+        }
+        return isfinite(mm) && sig > 0.f && isfinite(sig);
+    };
+    if constexpr (H16) {
+        if (qseed) h16_on = h16_enable();  // seeded lists: fp16 from the first tile
+    }
+
     for (int t = 0; t < ntiles; ++t) {
         ring.wait_full(t);
         const int o = ring.slot(t) * TILE;
@@ -452,40 +501,7 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
         }
         if (seed && t == 0) st.seed_lists(k0);  // home tile scanned: lists := seed copies
         if constexpr (H16) {
-            if (!h16_on && t + 1 < ntiles) {  // every list finite: fix the scale, switch to fp16
-                bool fin = true;
-#pragma unroll
-                for (int q = 0; q < Q; ++q) fin &= !valid[q] || st.buf[q][K - 1] < pos_inf<float>();
-                if (__syncthreads_and(fin)) {
-                    float m = 0.f;  // largest |q - C| and k-th distance over the CTA (non-negative)
-#pragma unroll
-                    for (int q = 0; q < Q; ++q)
-                        if (valid[q]) {
-                            const float dx = qx[q] - Cx, dy = qy[q] - Cy;
-                            m = fmaxf(m, fmaxf(sqrtf(dx * dx + dy * dy), sqrtf((float)st.buf[q][K - 1])));
-                        }
-                    if (threadIdx.x == 0) hred[0] = 0u;
-                    __syncthreads();
-                    atomicMax(&hred[0], __float_as_uint(m * 1.001f));
-                    __syncthreads();
-                    const float mm = __uint_as_float(hred[0]);
-                    int e = 0;
-                    frexpf(kH16Radius / fmaxf(mm, 0x1p-100f), &e);  // 16/m = f 2^e, f in [0.5, 1)
-                    e = e - 1 < -100 ? -100 : (e - 1 > 100 ? 100 : e - 1);
-                    sig = ldexpf(1.0f, e);  // sigma m <= 16
-                    h16_on = isfinite(mm) && sig > 0.f && isfinite(sig);
-#pragma unroll
-                    for (int q = 0; q < Q; ++q) {
-                        const float ax = -2.0f * __fmul_rn(__fsub_rn(qx[q], Cx), sig);
-                        const float by = -2.0f * __fmul_rn(__fsub_rn(qy[q], Cy), sig);
-                        h16.A[q] = __float2half2_rn(ax);
-                        h16.B[q] = __float2half2_rn(by);
-                        h16.T[q] = valid[q] ? h16_threshold(st.buf[q][K - 1], qx[q], qy[q], Cx, Cy, sig,
-                                                            h16.A[q], h16.B[q])
-                                            : -pos_inf<float>();
-                    }
-                }
-            }
+            if (!h16_on && t + 1 < ntiles) h16_on = h16_enable();
         }
         ring.release(t, ntiles, issue);
     }
@@ -596,6 +612,13 @@ static bool seed_unordered()
 
 // H16 (fp32, spatially ordered batches only): the fp16 pre-filter kernels; AIDW_KNN_H16=0
 // turns them off (tests compare both).
+// Ordered fp16 kernels seed lists per query (AIDW_KNN_QSEED=0: the home-tile seed).
+static bool knn_qseed_enabled()
+{
+    const char *e = getenv("AIDW_KNN_QSEED");
+    return !(e && e[0] == '0');
+}
+
 static int knn_h16_mode()
 {
     const char *e = getenv("AIDW_KNN_H16");
@@ -634,6 +657,10 @@ static int launch_knn_filter_t(KnnArgs<T> a, const FilterArgs &f, cudaStream_t s
             fo.pp = c + 5 * a.ndp;
             fo.px = c + 6 * a.ndp;
             fo.py = c + 7 * a.ndp;
+            if (H16 && knn_qseed_enabled()) {  // per-query seeds from the sorted copy
+                fo.sx = fo.px;
+                fo.sy = fo.py;
+            }
             if (fd->coords64) {  // fp64 handles: the sorted fp64 coordinates for the re-check
                 fo.px64 = fd->coords64;
                 fo.py64 = fd->coords64 + a.ndp;
