@@ -1,0 +1,128 @@
+"""CPU property test of the fp16 kNN pre-filter's rounding margin (DESIGN.md §4.1,
+passes.cuh h16_threshold / h16_convert / knn_h16_tile).
+
+The fp16 stage may only drop pairs that cannot enter a query's list: every TRUE
+candidate (canonical fp32 squared distance s < v, the list's k-th value) must give
+t̂ <= T.  This test emulates the kernel's operations bit for bit on the CPU -- fp32
+subtraction and scaling, fp16 rounding of the coordinates, p̂p rounded through fp32 to
+fp16, the two fp16 FMAs (the exact product + sum of fp16 operands is exact in fp64, then
+ONE rounding to fp16) -- and checks t̂ <= T on adversarial candidates: points just inside
+the k-th distance, at every angle, for queries anywhere in the CTA's region, at the scales
+the kernel picks (sigma m <= 16) and at extreme magnitudes (tiny and large coordinates,
+subnormal fp16 values).  T is the margin formula of h16_threshold, restated here (the
+GPU bit-identity tests exercise the CUDA code itself).
+"""
+import math
+from fractions import Fraction
+
+import numpy as np
+
+f16, f32 = np.float16, np.float32
+U16 = 2.0 ** -11
+UP = 2.0 ** -11 + 2.0 ** -22
+
+
+def fl32(x):
+    return float(f32(x))
+
+
+def fma32(a, b, c):
+    """fp32 fma: the exact a*b + c rounded once (Fraction -> nearest fp64 is exact for
+    these magnitudes only up to 53 bits, so round the exact value straight to fp32)."""
+    ex = Fraction(a) * Fraction(b) + Fraction(c)
+    lo = f32(float(ex))  # nearest fp64, then fp32: fix a possible double rounding below
+    cand = [lo, np.nextafter(lo, f32(-np.inf)), np.nextafter(lo, f32(np.inf))]
+    return float(min(cand, key=lambda z: (abs(Fraction(float(z)) - ex), int(np.float32(z).view(np.uint32)) & 1)))
+
+
+def fl16(x):
+    return float(f16(x))
+
+
+def fma16(a, b, c):
+    # a, b, c are fp16 values: a*b + c is exact in fp64, then one rounding
+    return fl16(a * b + c)
+
+
+def convert(x, y, cx, cy, sig):
+    """h16_convert: fp32 x - C_x, times sigma (exact), clamp, fp16; p̂p via fp32."""
+    u = fl16(min(max(fl32(fl32(x - cx) * sig), -256.0), 256.0))
+    v = fl16(min(max(fl32(fl32(y - cy) * sig), -256.0), 256.0))
+    pp = fl16(min(fma32(u, u, fl32(v * v)), 32768.0))
+    return u, v, pp
+
+
+def coeffs(qx, qy, cx, cy, sig):
+    a = fl16(-2.0 * fl32(fl32(qx - cx) * sig))
+    b = fl16(-2.0 * fl32(fl32(qy - cy) * sig))
+    return a, b
+
+
+def threshold(v, qx, qy, cx, cy, sig, a, b):
+    """h16_threshold (passes.cuh), restated."""
+    if not v < math.inf:
+        return math.inf
+    dx, dy = qx - cx, qy - cy
+    qn = sig * math.sqrt(dx * dx + dy * dy) * (1.0 + 2.0 ** -40)
+    r = sig * math.sqrt(v * (1.0 + 2.0 ** -20))
+    ah, bh = 0.5 * a, 0.5 * b
+    qq = ah * ah + bh * bh
+    qb = max(qn, math.sqrt(qq)) * (1.0 + UP)
+    d = UP * (2.0 * qb + r)
+    p = qb + r + d
+    rr = r + d
+    t = rr * rr - qq + UP * p * p + 1.002 * U16 * (p * p + qb * qb + rr * rr) + 2.0 ** -18
+    return float(np.nextafter(f32(t), f32(np.inf)))  # __double2float_ru (upper bound)
+
+
+def canon32(qx, qy, px, py):
+    dx = fl32(qx - px)
+    dy = fl32(qy - py)
+    return fma32(dx, dx, fl32(dy * dy))
+
+
+def check_case(rng, scale, n_q=40, n_p=60):
+    """A CTA region of radius ~scale around C, queries inside, k-th distance ~ kth."""
+    cx = fl32(rng.uniform(-3, 3) * scale * 50)
+    cy = fl32(rng.uniform(-3, 3) * scale * 50)
+    qs = [(fl32(cx + rng.uniform(-1, 1) * scale), fl32(cy + rng.uniform(-1, 1) * scale)) for _ in range(n_q)]
+    kth = scale * 10 ** rng.uniform(-2.5, 0.3)  # k-th distance relative to the region
+    vs = [fl32((kth * rng.uniform(0.5, 1.5)) ** 2) for _ in qs]
+    m = max(max(math.hypot(qx - cx, qy - cy), math.sqrt(v)) for (qx, qy), v in zip(qs, vs)) * 1.001
+    e = math.frexp(16.0 / m)[1] - 1
+    sig = 2.0 ** max(-100, min(100, e))
+    worst = -math.inf
+    for (qx, qy), v in zip(qs, vs):
+        a, b = coeffs(qx, qy, cx, cy, sig)
+        T = threshold(v, qx, qy, cx, cy, sig, a, b)
+        for _ in range(n_p):
+            ang = rng.uniform(0, 2 * math.pi)
+            rad = math.sqrt(v) * (1.0 - 10 ** rng.uniform(-7, -0.3))  # just inside, mostly
+            px, py = fl32(qx + rad * math.cos(ang)), fl32(qy + rad * math.sin(ang))
+            if not canon32(qx, qy, px, py) < v:
+                continue  # not a true candidate after rounding
+            u, w, pp = convert(px, py, cx, cy, sig)
+            t = fma16(b, w, fma16(a, u, pp))
+            worst = max(worst, t - T)
+            assert t <= T, (qx, qy, px, py, v, t, T)
+    return worst
+
+
+def test_h16_margin_keeps_every_candidate():
+    rng = np.random.default_rng(2024)
+    for scale in (1e-2, 2e-2, 1.0, 3e-5, 7e3):
+        for _ in range(12):
+            check_case(rng, scale)
+
+
+def test_h16_margin_is_not_vacuous():
+    """The margin is tight enough to be useful: for a typical C4 CTA (region radius ~9
+    k-th distances) T exceeds the exact scaled threshold by well under the threshold."""
+    cx = cy = 0.5
+    qx, qy = fl32(0.5 + 0.016), fl32(0.5)
+    v = fl32(0.0018 ** 2)
+    sig = 2.0 ** (math.frexp(16.0 / (0.016 * 1.001))[1] - 1)
+    a, b = coeffs(qx, qy, cx, cy, sig)
+    T = threshold(v, qx, qy, cx, cy, sig, a, b)
+    exact = sig * sig * v - (0.5 * a) ** 2 - (0.5 * b) ** 2
+    assert 0 < T - exact < 0.5 * sig * sig * v
