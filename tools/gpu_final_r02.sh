@@ -15,5 +15,9 @@ AIDW_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --
 timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > $O/bench_ref.json 2>> $O/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
     python bench.py --profile --warmup 1 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"knn_filter" -c 1 -o $O/prof_knn python bench.py --profile --warmup 0 > $O/ncu_knn.log 2>&1
+python tools/ncu_summary.py $O/prof_knn.ncu-rep --json $O/ncu_knn_summary.json > /dev/null 2>&1
+XM=sm__inst_executed_pipe_xu.sum,sm__inst_executed_pipe_fmaheavy.sum,sm__inst_executed_pipe_fmalite.sum,sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fmalite_cycles_active.avg.pct_of_peak_sustained_active,sm__cycles_active.avg,sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active,gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
+timeout 600 ncu --metrics $XM --clock-control none -k regex:"interp_f32x2|knn_filter" -c 2 --csv --page raw python bench.py --profile --warmup 0 > $O/ncu_xu.csv 2> $O/ncu_xu.err
 timeout 1200 python tools/table1.py --out $O/table1.md --json $O/table1.jsonl > $O/table1.log 2>&1
 echo done
