@@ -622,8 +622,8 @@ static bool knn_qseed_enabled()
 static int knn_h16_mode()
 {
     const char *e = getenv("AIDW_KNN_H16");
-    // 0 off, 1 register-capped (128 registers, 4 CTAs/SM; C4 kNN 85.9 ms), 2 uncapped
-    // (168 registers, 3 CTAs/SM; 90.4 ms) -- profiles/r02_tune_knn_h16.log
+    // 0 off, 1 default (size-dependent shape, uncapped registers), 2 Q = 4 uncapped at every
+    // size, 3 register-capped -- profiles/r02_tune_knn_h16.log, r02_tune_knn_shapes_qseed.log
     return e ? atoi(e) : 1;
 }
 
@@ -749,6 +749,9 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
         case 25: return launch_knn_filter_t<10, 2, 32, 0, float, true>(a, f, st, sp, fd);  // fp16, Q = 2
         case 26: return launch_knn_filter_t<10, 2, 32, 6, float, true>(a, f, st, sp, fd);  // fp16, Q = 2, 6 CTAs/SM
         case 27: return launch_knn_filter_t<10, 3, 32, 5, float, true>(a, f, st, sp, fd);  // fp16, Q = 3
+        case 28: return launch_knn_filter_t<10, 2, 32, 8, float, true>(a, f, st, sp, fd);  // fp16, Q = 2, 8 CTAs/SM
+        case 29: return launch_knn_filter_t<10, 4, 32, 5, float, true>(a, f, st, sp, fd);  // fp16, Q = 4, 5 CTAs/SM
+        case 30: return launch_knn_filter_t<10, 2, 32, 7, float, true>(a, f, st, sp, fd);  // fp16, Q = 2, 7 CTAs/SM
         default: break;
         }
     }
@@ -760,9 +763,12 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
     if (k <= 10) {  // large (spatially ordered) batches: Q = 4, G = 32 (108 vs 115 ms at C4)
         if (order_queries(a.nq) && a.nq >= 32768) {
             switch (knn_h16_mode()) {
-            case 1:  // Q = 2 (6 CTAs/SM) below ~384K queries (strong-scaled shares): 128,000
-                     // 13.8 -> 13.0 ms, 32,768 7.1 -> 6.1; Q = 4 above (C4 86.8 vs 89.2 ms)
-                     // -- profiles/r02_tune_knn_h16_q.log
+            case 1:  // Q = 2 below ~384K queries (strong-scaled shares), Q = 4 above; with the
+                     // per-query seeds the uncapped shapes win (C4 82.6 vs 83.6 ms capped,
+                     // 128,000 queries 11.7 vs 12.0) -- profiles/r02_tune_knn_shapes_qseed.log
+                if (a.nq < 393216) return launch_knn_filter_t<10, 2, 32, 0, float, true>(a, f, st, sp, fd);
+                return launch_knn_filter_t<10, 4, 32, 0, float, true>(a, f, st, sp, fd);
+            case 3:  // the register-capped shapes (4 / 6 CTAs/SM), the round-2 default before the seeds
                 if (a.nq < 393216) return launch_knn_filter_t<10, 2, 32, 6, float, true>(a, f, st, sp, fd);
                 return launch_knn_filter_t<10, 4, 32, 4, float, true>(a, f, st, sp, fd);
             case 2: return launch_knn_filter_t<10, 4, 32, 0, float, true>(a, f, st, sp, fd);

@@ -235,7 +235,7 @@ def test_coincident_queries(P, orc, dtype):
 
 @pytest.mark.parametrize("case,k", [("uniform", 10), ("clustered", 10), ("offset", 10), ("tiny", 10),
                                     ("outliers", 10), ("clustered", 15), ("outliers", 15)])
-@pytest.mark.parametrize("h16", ["1", "2"])
+@pytest.mark.parametrize("h16", ["1", "2", "3"])
 def test_knn_h16_bit_identical(P, orc, monkeypatch, case, k, h16):
     """The fp16 pre-filter of spatially ordered fp32 batches (passes.cuh knn_h16_tile; its
     threshold carries a rigorous rounding margin) never drops a true candidate: lists,
