@@ -1,7 +1,16 @@
-# GPU check (r02u): default fp16 kNN shapes -- tests + sizes
+# GPU A/B (r02v): ring refill by the last releasing warp (libaidw_ringlast.so) vs thread 0
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/${1:-r02u}
+O=gpurun_out/${1:-r02v}
 mkdir -p $O
-timeout 1200 python -m pytest tests/test_gpu.py -q -rf -k "h16 or golden and C4 or graph or order or seed or split or C3" > $O/pytest.log 2>&1; echo rc=$? >> $O/pytest.log
-for nq in 1024000 512000 256000 128000 32768; do timeout 120 python tools/tune_knn.py $nq >> $O/tune_knn.log 2>&1; done
+cp paper_1511_02186_b200/libaidw.so /tmp/libaidw_A.so
+for lib in A B; do
+  if [ $lib = B ]; then cp paper_1511_02186_b200/libaidw_ringlast.so paper_1511_02186_b200/libaidw.so; fi
+  echo "== $lib" >> $O/ab.log
+  timeout 120 python tools/tune_knn.py >> $O/ab.log 2>&1
+  timeout 120 python tools/tune_knn.py 128000 >> $O/ab.log 2>&1
+  timeout 120 python tools/tune_interp.py >> $O/ab.log 2>&1
+  timeout 120 python tools/tune_interp.py 128000 >> $O/ab.log 2>&1
+  if [ $lib = B ]; then timeout 900 python -m pytest tests/test_gpu.py -q -x -k "not C5" > $O/pytest_B.log 2>&1; echo rc=$? >> $O/pytest_B.log; fi
+done
+cp /tmp/libaidw_A.so paper_1511_02186_b200/libaidw.so
 echo done
