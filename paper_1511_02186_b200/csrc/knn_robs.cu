@@ -407,11 +407,12 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
 
     // fp16 pre-filter state (H16): the CTA's query-bbox centre, the scale, per-query
     // coefficients and thresholds; enabled once every query has a finite k-th distance
-    __shared__ __align__(16) __half2 hbuf[H16 ? 2 : 1][3][H16 ? TILE / 2 : 1];
+    __shared__ __align__(16) __half2 hbuf[H16 ? 2 : 1][4][H16 ? TILE / 2 : 1];
     __shared__ unsigned hred[4];
     KnnH16<Q> h16;
     float Cx = 0.f, Cy = 0.f, sig = 0.f;
     bool h16_on = false;
+    int axis = -1;  // strip axis: the one along which the CTA's queries spread least
     if constexpr (H16) {
         // centre of the CTA's valid queries (order-preserving keys of the fp32 values)
         auto key = [](float v) { const unsigned b = __float_as_uint(v); return (b >> 31) ? ~b : b | 0x80000000u; };
@@ -430,6 +431,7 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
         if (hred[0] != 0xffffffffu) {
             Cx = 0.5f * unkey(hred[0]) + 0.5f * unkey(hred[1]);
             Cy = 0.5f * unkey(hred[2]) + 0.5f * unkey(hred[3]);
+            if (f.strip) axis = unkey(hred[3]) - unkey(hred[2]) < unkey(hred[1]) - unkey(hred[0]) ? 1 : 0;
         }
         __syncthreads();  // hred is reused for the scale
     }
@@ -462,10 +464,13 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
         for (int q = 0; q < Q; ++q) {
             const float ax = -2.0f * __fmul_rn(__fsub_rn(qx[q], Cx), sig);
             const float by = -2.0f * __fmul_rn(__fsub_rn(qy[q], Cy), sig);
-            h16.A[q] = __float2half2_rn(ax);
-            h16.B[q] = __float2half2_rn(by);
-            h16.T[q] = valid[q] ? h16_threshold(st.buf[q][K - 1], qx[q], qy[q], Cx, Cy, sig, h16.A[q], h16.B[q])
-                                : -pos_inf<float>();
+            // the strip axis' coefficient goes first (h16_convert swaps û, v̂ likewise)
+            h16.A[q] = __float2half2_rn(axis == 1 ? by : ax);
+            h16.B[q] = __float2half2_rn(axis == 1 ? ax : by);
+            const float v = st.buf[q][K - 1];
+            h16.T[q] = !valid[q] ? -pos_inf<float>()
+                       : axis < 0 ? h16_threshold<false>(v, qx[q], qy[q], Cx, Cy, sig, h16.A[q], h16.B[q])
+                                  : h16_threshold<true>(v, qx[q], qy[q], Cx, Cy, sig, h16.A[q], h16.B[q]);
         }
         return isfinite(mm) && sig > 0.f && isfinite(sig);
     };
@@ -479,10 +484,15 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
         if constexpr (H16) {
             if (h16_on) {
                 __half2 *hb = &hbuf[t & 1][0][0];
-                h16_convert<TILE>(spx + o, spy + o, hb, hb + TILE / 2, hb + TILE, Cx, Cy, sig);
+                h16_convert<TILE>(spx + o, spy + o, hb, hb + TILE / 2, hb + TILE, hb + 3 * TILE / 2, axis, Cx, Cy,
+                                  sig);
                 __syncthreads();
-                knn_h16_tile<K, Q, G, TILE>(st, h16, hb, hb + TILE / 2, hb + TILE, scx + o, scy + o, spp + o,
-                                            spx + o, spy + o, Cx, Cy, sig);
+                if (axis >= 0)
+                    knn_h16_tile<K, Q, G, TILE, true>(st, h16, hb, hb + TILE / 2, hb + TILE, hb + 3 * TILE / 2,
+                                                      scx + o, scy + o, spp + o, spx + o, spy + o, Cx, Cy, sig);
+                else
+                    knn_h16_tile<K, Q, G, TILE, false>(st, h16, hb, hb + TILE / 2, hb + TILE, hb + 3 * TILE / 2,
+                                                       scx + o, scy + o, spp + o, spx + o, spy + o, Cx, Cy, sig);
             } else {  // warm-up tile (lists not yet finite): every group straight to the rare
                       // path -- with an infinite threshold the filter passes every pair anyway --
                       // so the kernel carries no fp32 main loop (registers)
@@ -619,6 +629,13 @@ static bool knn_qseed_enabled()
     return !(e && e[0] == '0');
 }
 
+// AIDW_KNN_STRIP=0: the fp16 kernels run the 2-D test on every group (no strip pre-test).
+static int knn_strip_enabled()
+{
+    const char *e = getenv("AIDW_KNN_STRIP");
+    return (e && e[0] == '0') ? 0 : 1;
+}
+
 static int knn_h16_mode()
 {
     const char *e = getenv("AIDW_KNN_H16");
@@ -647,6 +664,7 @@ static int launch_knn_filter_t(KnnArgs<T> a, const FilterArgs &f, cudaStream_t s
                                              (int)(a.ndp / kTileKF), a, sp);
     int pre = 0;
     FilterArgs fo = f;
+    fo.strip = knn_strip_enabled();
     if (ordered) {
         pre = launch_order_queries(a.qx, a.qy, a.nq, fd, &fd->qorder, &a.perm, st);
         if (pre < 0) return -1;
@@ -752,6 +770,7 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
         case 28: return launch_knn_filter_t<10, 2, 32, 8, float, true>(a, f, st, sp, fd);  // fp16, Q = 2, 8 CTAs/SM
         case 29: return launch_knn_filter_t<10, 4, 32, 5, float, true>(a, f, st, sp, fd);  // fp16, Q = 4, 5 CTAs/SM
         case 30: return launch_knn_filter_t<10, 2, 32, 7, float, true>(a, f, st, sp, fd);  // fp16, Q = 2, 7 CTAs/SM
+        case 31: return launch_knn_filter_t<10, 4, 32, 3, float, true>(a, f, st, sp, fd);  // fp16, Q = 4, 3 CTAs/SM
         default: break;
         }
     }
@@ -764,10 +783,11 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
         if (order_queries(a.nq) && a.nq >= 32768) {
             switch (knn_h16_mode()) {
             case 1:  // Q = 2 below ~384K queries (strong-scaled shares), Q = 4 above; with the
-                     // per-query seeds the uncapped shapes win (C4 82.6 vs 83.6 ms capped,
-                     // 128,000 queries 11.7 vs 12.0) -- profiles/r02_tune_knn_shapes_qseed.log
+                     // strip pre-test (round 2) Q = 4 at 3 CTAs/SM (C4 59.4 ms; uncapped,
+                     // 193 registers: 64.9) and Q = 2 uncapped below (128,000 queries 9.0 ms)
+                     // -- profiles/r02_tune_knn_strip_a.log
                 if (a.nq < 393216) return launch_knn_filter_t<10, 2, 32, 0, float, true>(a, f, st, sp, fd);
-                return launch_knn_filter_t<10, 4, 32, 0, float, true>(a, f, st, sp, fd);
+                return launch_knn_filter_t<10, 4, 32, 3, float, true>(a, f, st, sp, fd);
             case 3:  // the register-capped shapes (4 / 6 CTAs/SM), the round-2 default before the seeds
                 if (a.nq < 393216) return launch_knn_filter_t<10, 2, 32, 6, float, true>(a, f, st, sp, fd);
                 return launch_knn_filter_t<10, 4, 32, 4, float, true>(a, f, st, sp, fd);

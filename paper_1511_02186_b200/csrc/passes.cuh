@@ -101,6 +101,7 @@ struct FilterArgs {
     // (KnnF32State::seed_query); null = no seed
     const float *sx = nullptr, *sy = nullptr;
     const double *sx64 = nullptr, *sy64 = nullptr;
+    int strip = 1;  // fp16 kernels: 1 = strip pre-test, 0 = the 2-D test only
 };
 
 // thr_of: the filter threshold for the canonical k-th distance thr, in fp32 with every
@@ -344,7 +345,8 @@ __device__ __forceinline__ void knn_f32_tile(KnnF32State<K, Q, T> &st, const flo
 // land at t̂ >= 16384, far above T.
 template <int Q> struct KnnH16 {
     __half2 A[Q], B[Q];  // splats of fl16(-2 sigma (q - C))
-    float T[Q];          // fp16-stage threshold (t scale, fp32, rounded up); -inf for empty slots
+    float T[Q];          // STRIP threshold on the strip axis' t scale (fp32, rounded up; the
+                         // 2-D threshold is derived from it, h16_t2d); -inf for empty slots
 };
 
 constexpr float kH16Clamp = 256.0f, kH16PPClamp = 32768.0f, kH16Radius = 16.0f;
@@ -357,6 +359,13 @@ constexpr float kH16Clamp = 256.0f, kH16PPClamp = 32768.0f, kH16Radius = 16.0f;
 // + 2^-18 (absolute slack: fp16 subnormal coordinates and results, <= 2^-25 each; sigma
 // keeps the candidates' scaled magnitudes O(1..32), so this is far below T).  |q̂|² is exact
 // from the fp16 coefficients.
+// Round 2 (the strip pre-test): the function returns the threshold of the ONE-axis test
+// t̂1 = p̂s + Ŝ ŝ (ŝ = û for AXIS 0, v̂ for AXIS 1; p̂s = fl16(ŝ²)): a true candidate is
+// within R = r + Delta of the query along that axis too, and every rounding term of the
+// 2-D bound dominates its one-axis counterpart, so the same formula with |q̂|² replaced by
+// the strip axis' share â² (A is the strip axis' coefficient) bounds t̂1.  The 2-D
+// threshold is T1 - b̂², rounded up (h16_t2d).  !STRIP: the 2-D threshold itself.
+template <bool STRIP>
 __device__ __forceinline__ float h16_threshold(float v, float qx, float qy, float Cx, float Cy, float sig,
                                                __half2 A, __half2 B)
 {
@@ -370,15 +379,28 @@ __device__ __forceinline__ float h16_threshold(float v, float qx, float qy, floa
     const double Qb = fmax(Qn, sqrt(qq)) * (1.0 + up);
     const double D = up * (2.0 * Qb + r);
     const double P = Qb + r + D, R = r + D;
-    const double T = R * R - qq + up * P * P + 1.002 * u16 * (P * P + Qb * Qb + R * R) + 0x1p-18;
+    const double T = R * R - (STRIP ? ah * ah : qq) + up * P * P + 1.002 * u16 * (P * P + Qb * Qb + R * R) +
+                     0x1p-18;
     return __double2float_ru(T);
 }
 
-// One tile's fp16 copy: TILE/2 couples of (û, v̂, p̂p), all threads of the CTA.
+// The 2-D test's threshold from the strip threshold T1: T1 - (B/2)², the product exact in
+// fp32 (11-bit operands), one upward rounding.
+__device__ __forceinline__ float h16_t2d(float T1, __half2 B)
+{
+    const float o = 0.5f * __low2float(B);
+    return __fmaf_ru(-o, o, T1);
+}
+
+// One tile's fp16 copy: TILE/2 couples of (û, v̂, p̂p) and the strip squares p̂s = fl16(û²)
+// (exact in fp32 before the rounding: 11-bit operands), all threads of the CTA.  With
+// axis == 1 the CTA's strip axis is y: û and v̂ trade places (so do the query
+// coefficients, knn_filter_kernel), t̂ is symmetric in the two.
 template <int TILE>
 __device__ __forceinline__ void h16_convert(const float *__restrict__ tpx, const float *__restrict__ tpy,
                                             __half2 *__restrict__ hu, __half2 *__restrict__ hv,
-                                            __half2 *__restrict__ hp, float Cx, float Cy, float sig)
+                                            __half2 *__restrict__ hp, __half2 *__restrict__ hs, int axis,
+                                            float Cx, float Cy, float sig)
 {
     for (int i = threadIdx.x; i < TILE / 2; i += blockDim.x) {
         const float2 x = *reinterpret_cast<const float2 *>(tpx + 2 * i);
@@ -387,28 +409,40 @@ __device__ __forceinline__ void h16_convert(const float *__restrict__ tpx, const
         const float u1 = fminf(fmaxf(__fmul_rn(__fsub_rn(x.y, Cx), sig), -kH16Clamp), kH16Clamp);
         const float v0 = fminf(fmaxf(__fmul_rn(__fsub_rn(y.x, Cy), sig), -kH16Clamp), kH16Clamp);
         const float v1 = fminf(fmaxf(__fmul_rn(__fsub_rn(y.y, Cy), sig), -kH16Clamp), kH16Clamp);
-        const __half2 U = __floats2half2_rn(u0, u1), V = __floats2half2_rn(v0, v1);
+        __half2 U = __floats2half2_rn(u0, u1), V = __floats2half2_rn(v0, v1);
+        if (axis == 1) {  // the strip axis always goes first (the coefficients are swapped too)
+            const __half2 w = U;
+            U = V;
+            V = w;
+        }
         const float2 uf = __half22float2(U), vf = __half22float2(V);
         const float p0 = fminf(__fmaf_rn(uf.x, uf.x, __fmul_rn(vf.x, vf.x)), kH16PPClamp);
         const float p1 = fminf(__fmaf_rn(uf.y, uf.y, __fmul_rn(vf.y, vf.y)), kH16PPClamp);
         hu[i] = U;
         hv[i] = V;
         hp[i] = __floats2half2_rn(p0, p1);
+        hs[i] = __floats2half2_rn(fminf(__fmul_rn(uf.x, uf.x), kH16PPClamp), fminf(__fmul_rn(uf.y, uf.y), kH16PPClamp));
     }
 }
 
 // The fp16 main loop over one tile (same groups, votes and rare path as knn_f32_tile).
-template <int K, int Q, int G, int TILE>
+// STRIP (round 2, DESIGN.md §4.1 "strip pre-test"): every group of G points is first
+// tested on ONE axis (the first, h16_convert), t̂1 = p̂s + Â û (one HFMA2 per couple instead
+// of two: 1.6x the pairs per clock, tools/knn_loop_bench.cu); only a group that some
+// lane's strip test keeps runs the 2-D test, and only a group that passes both reaches
+// the rare path.  Both tests are necessary conditions of a true candidate, so the
+// selected multiset is unchanged.  !STRIP: the 2-D test alone (AIDW_KNN_STRIP=0).
+template <int K, int Q, int G, int TILE, bool STRIP>
 __device__ __forceinline__ void knn_h16_tile(KnnF32State<K, Q, float> &st, KnnH16<Q> &h, const __half2 *hu,
-                                             const __half2 *hv, const __half2 *hp, const float *__restrict__ tcx,
-                                             const float *__restrict__ tcy, const float *__restrict__ tpp,
-                                             const float *__restrict__ tpx, const float *__restrict__ tpy,
-                                             float Cx, float Cy, float sig)
+                                             const __half2 *hv, const __half2 *hp, const __half2 *hs,
+                                             const float *__restrict__ tcx, const float *__restrict__ tcy,
+                                             const float *__restrict__ tpp, const float *__restrict__ tpx,
+                                             const float *__restrict__ tpy, float Cx, float Cy, float sig)
 {
     static_assert(G % 8 == 0 && G <= 32 && TILE % G == 0, "group size");
-    const uint32_t au = smem_addr(hu), av = smem_addr(hv), ap = smem_addr(hp);
-#pragma unroll 1
-    for (int j = 0; j < TILE; j += G) {
+    const uint32_t au = smem_addr(hu), av = smem_addr(hv), ap = smem_addr(hp), aps = smem_addr(hs);
+    // the 2-D test of group j: per-query flags (AND-ed into hq) and the warp vote
+    auto test2d = [&](int j, bool (&hq)[Q]) -> bool {
         __half2 mn[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) mn[q] = __half2half2(__ushort_as_half((unsigned short)0x7c00));  // +inf
@@ -427,16 +461,54 @@ __device__ __forceinline__ void knn_h16_tile(KnnF32State<K, Q, float> &st, KnnH1
                 mn[q] = __hmin2(__hmin2(__hmin2(t[0], t[1]), __hmin2(t[2], t[3])), mn[q]);
             }
         }
-        bool hq[Q], hit = false;
+        bool hit = false;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             const float2 m = __half22float2(mn[q]);
-            hq[q] = fminf(m.x, m.y) <= h.T[q];
+            const float T2 = STRIP ? h16_t2d(h.T[q], h.B[q]) : h.T[q];
+            hq[q] = hq[q] && fminf(m.x, m.y) <= T2;
             hit |= hq[q];
         }
-        if (__any_sync(0xffffffffu, hit))
+        return __any_sync(0xffffffffu, hit);
+    };
+#pragma unroll 1
+    for (int j = 0; j < TILE; j += G) {
+        bool hq[Q];
+        bool go;
+        if constexpr (!STRIP) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) hq[q] = true;
+            go = test2d(j, hq);
+        } else {
+            __half2 mn[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) mn[q] = __half2half2(__ushort_as_half((unsigned short)0x7c00));  // +inf
+#pragma unroll
+            for (int c = 0; c < G; c += 8) {
+                const uint32_t o = (uint32_t)(j + c) * 2u;
+                const float4 S4 = lds128(au + o), P4 = lds128(aps + o);
+                const __half2 *sv = reinterpret_cast<const __half2 *>(&S4);
+                const __half2 *ps = reinterpret_cast<const __half2 *>(&P4);
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    __half2 t[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) t[e] = __hfma2(h.A[q], sv[e], ps[e]);
+                    mn[q] = __hmin2(__hmin2(__hmin2(t[0], t[1]), __hmin2(t[2], t[3])), mn[q]);
+                }
+            }
+            bool hit = false;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const float2 m = __half22float2(mn[q]);
+                hq[q] = fminf(m.x, m.y) <= h.T[q];
+                hit |= hq[q];
+            }
+            go = __any_sync(0xffffffffu, hit) && test2d(j, hq);
+        }
+        if (go)
             knn_rare_group_impl<K, Q, G>(st, hq, tcx, tcy, tpp, tpx, tpy, j, [&](int q) {
-                h.T[q] = h16_threshold(st.buf[q][K - 1], st.qx[q], st.qy[q], Cx, Cy, sig, h.A[q], h.B[q]);
+                h.T[q] = h16_threshold<STRIP>(st.buf[q][K - 1], st.qx[q], st.qy[q], Cx, Cy, sig, h.A[q], h.B[q]);
             });
     }
 }

@@ -58,8 +58,9 @@ def coeffs(qx, qy, cx, cy, sig):
     return a, b
 
 
-def threshold(v, qx, qy, cx, cy, sig, a, b):
-    """h16_threshold (passes.cuh), restated."""
+def threshold(v, qx, qy, cx, cy, sig, a, b, strip=False):
+    """h16_threshold<STRIP> (passes.cuh), restated: the 2-D threshold, or with strip=True
+    the one-axis (strip) threshold of the axis whose coefficient is `a`."""
     if not v < math.inf:
         return math.inf
     dx, dy = qx - cx, qy - cy
@@ -71,8 +72,29 @@ def threshold(v, qx, qy, cx, cy, sig, a, b):
     d = UP * (2.0 * qb + r)
     p = qb + r + d
     rr = r + d
-    t = rr * rr - qq + UP * p * p + 1.002 * U16 * (p * p + qb * qb + rr * rr) + 2.0 ** -18
-    return float(np.nextafter(f32(t), f32(np.inf)))  # __double2float_ru (upper bound)
+    t = rr * rr - (ah * ah if strip else qq) + UP * p * p + 1.002 * U16 * (p * p + qb * qb + rr * rr) + 2.0 ** -18
+    return ru32(t)  # __double2float_ru (upper bound)
+
+
+def ru32(t):
+    """fp64 -> fp32 rounded up (an upper bound of t)."""
+    f = f32(t)
+    return float(f) if float(f) >= t else float(np.nextafter(f, f32(np.inf)))
+
+
+def t2d(T1, b):
+    """h16_t2d: T1 - (b/2)^2, the product exact, ONE upward rounding to fp32."""
+    ex = Fraction(T1) - Fraction(0.5 * b) ** 2
+    lo = f32(float(ex))
+    for z in (np.nextafter(lo, f32(-np.inf)), lo, np.nextafter(lo, f32(np.inf))):
+        if Fraction(float(z)) >= ex:
+            return float(z)
+    raise AssertionError
+
+
+def strip_convert(s):
+    """h16_convert's strip square: p̂s = fl16(min(ŝ², 32768)) (ŝ² exact in fp32)."""
+    return fl16(min(fl32(s * s), 32768.0))
 
 
 def canon32(qx, qy, px, py):
@@ -96,7 +118,7 @@ def check_case(rng, scale, n_q=40, n_p=60):
         a, b = coeffs(qx, qy, cx, cy, sig)
         T = threshold(v, qx, qy, cx, cy, sig, a, b)
         for _ in range(n_p):
-            ang = rng.uniform(0, 2 * math.pi)
+            ang = rng.choice([0.0, 0.5 * math.pi, math.pi, 1.5 * math.pi]) if rng.uniform() < 0.3 else rng.uniform(0, 2 * math.pi)
             rad = math.sqrt(v) * (1.0 - 10 ** rng.uniform(-7, -0.3))  # just inside, mostly
             px, py = fl32(qx + rad * math.cos(ang)), fl32(qy + rad * math.sin(ang))
             if not canon32(qx, qy, px, py) < v:
@@ -105,6 +127,15 @@ def check_case(rng, scale, n_q=40, n_p=60):
             t = fma16(b, w, fma16(a, u, pp))
             worst = max(worst, t - T)
             assert t <= T, (qx, qy, px, py, v, t, T)
+            # the strip pre-test on either axis (knn_filter_kernel swaps the axes, and the
+            # coefficients with them, when the strip axis is y) and its derived 2-D threshold
+            for (c1, s1, c2, s2) in ((a, u, b, w), (b, w, a, u)):
+                T1 = threshold(v, qx, qy, cx, cy, sig, c1, c2, strip=True)
+                t1 = fma16(c1, s1, strip_convert(s1))
+                assert t1 <= T1, (qx, qy, px, py, v, t1, T1)
+                pp2 = fl16(min(fma32(s1, s1, fl32(s2 * s2)), 32768.0))
+                t2 = fma16(c2, s2, fma16(c1, s1, pp2))
+                assert t2 <= t2d(T1, c2), (qx, qy, px, py, v, t2, T1)
     return worst
 
 
@@ -126,3 +157,34 @@ def test_h16_margin_is_not_vacuous():
     T = threshold(v, qx, qy, cx, cy, sig, a, b)
     exact = sig * sig * v - (0.5 * a) ** 2 - (0.5 * b) ** 2
     assert 0 < T - exact < 0.5 * sig * sig * v
+
+
+def test_strip_margin_is_not_vacuous():
+    """The strip threshold of a typical C4 CTA keeps only a thin strip: a point at 3 k-th
+    distances from the query along the strip axis fails the one-axis test."""
+    cx = cy = 0.5
+    qx, qy = fl32(0.5 + 0.006), fl32(0.5 - 0.004)
+    v = fl32(0.0018 ** 2)
+    sig = 2.0 ** (math.frexp(16.0 / (0.011 * 1.001))[1] - 1)
+    a, b = coeffs(qx, qy, cx, cy, sig)
+    T1 = threshold(v, qx, qy, cx, cy, sig, a, b, strip=True)
+    u, _, _ = convert(fl32(qx + 3 * 0.0018), qy, cx, cy, sig)
+    assert fma16(a, u, strip_convert(u)) > T1
+
+
+def test_strip_mutation_detected():
+    """Dropping the margin terms from the strip threshold loses true candidates."""
+    rng = np.random.default_rng(7)
+    lost = 0
+    for _ in range(400):
+        cx, cy = 0.5, 0.5
+        qx, qy = fl32(0.5 + rng.uniform(-0.01, 0.01)), fl32(0.5 + rng.uniform(-0.01, 0.01))
+        v = fl32(0.0018 ** 2)
+        sig = 2.0 ** (math.frexp(16.0 / (0.0142 * 1.001))[1] - 1)
+        a, b = coeffs(qx, qy, cx, cy, sig)
+        r = sig * math.sqrt(v)
+        bare = r * r - (0.5 * a) ** 2  # no rounding terms
+        rad = math.sqrt(v) * (1 - 1e-6)
+        u, _, _ = convert(fl32(qx + rad * rng.choice([-1.0, 1.0])), qy, cx, cy, sig)
+        lost += fma16(a, u, strip_convert(u)) > bare
+    assert lost > 0

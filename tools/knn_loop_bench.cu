@@ -236,10 +236,95 @@ __global__ void __launch_bounds__(THREADS) knn_loop_h2(const float *__restrict__
     if (blockIdx.x == 0 && threadIdx.x == 0) *clk = Clk{c0, c1};
 }
 
+
+// VAR 10-13 (round 2, separate kernel): the strip (1-D) pre-test and integer min trees.
+// VAR 10: 1-D t = pu + A u (ONE HFMA2 per couple) + HMNMX2 tree (2 loads per 8 points)
+// VAR 11: 1-D t on HFMA2 + packed int16 3-input min (VIMNMX3.S16x2) on the bit patterns
+// VAR 12: 2-D t (two HFMA2 per couple, as VAR 7) + the VIMNMX3.S16x2 tree
+__device__ __forceinline__ unsigned h2u(__half2 h) { return *reinterpret_cast<unsigned *>(&h); }
+__device__ __forceinline__ unsigned vmin3(unsigned a, unsigned b, unsigned c)
+{
+    unsigned r;
+    asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(r), "r"(c));
+    return r;
+}
+template <int Q, int G, int VAR>
+__global__ void __launch_bounds__(THREADS) knn_loop_h1(const float *__restrict__ g, float *out, int reps, Clk *clk)
+{
+    extern __shared__ __align__(16) float sm[];
+    __half2 *hx = reinterpret_cast<__half2 *>(sm);  // TILE/2 couples each
+    __half2 *hy = hx + TILE / 2, *hp = hy + TILE / 2;
+    for (int i = threadIdx.x; i < TILE / 2; i += THREADS) {
+        hx[i] = __floats2half2_rn(g[2 * i], g[2 * i + 1]);
+        hy[i] = __floats2half2_rn(g[TILE + 2 * i], g[TILE + 2 * i + 1]);
+        hp[i] = __floats2half2_rn(g[2 * TILE + 2 * i], g[2 * TILE + 2 * i + 1]);
+    }
+    __syncthreads();
+    __half2 A[Q], B[Q];
+    float thr[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        A[q] = __float2half2_rn(opaque(-2.0f * (0.1f + 0.01f * q + 1e-6f * threadIdx.x)));
+        B[q] = __float2half2_rn(opaque(-2.0f * (0.3f - 0.01f * q)));
+        thr[q] = opaque(-1e30f);
+    }
+    float acc = 0.f;
+    unsigned long long c0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll 1
+        for (int j = 0; j < TILE / 2; j += G / 2) {
+            __half2 mn[Q];
+            unsigned mi[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                mn[q] = __float2half2_rn(60000.f);
+                mi[q] = 0x7bff7bffu;
+            }
+#pragma unroll
+            for (int c = 0; c < G / 2; c += 4) {  // 8 points = 4 couples
+                const uint4 X = *reinterpret_cast<const uint4 *>(hx + j + c);
+                const uint4 P = *reinterpret_cast<const uint4 *>(hp + j + c);
+                const __half2 *xv = reinterpret_cast<const __half2 *>(&X);
+                const __half2 *pv = reinterpret_cast<const __half2 *>(&P);
+                uint4 Y = make_uint4(0, 0, 0, 0);
+                if (VAR == 12) Y = *reinterpret_cast<const uint4 *>(hy + j + c);
+                const __half2 *yv = reinterpret_cast<const __half2 *>(&Y);
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    __half2 t[4];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h)
+                        t[h] = VAR == 12 ? __hfma2(B[q], yv[h], __hfma2(A[q], xv[h], pv[h])) : __hfma2(A[q], xv[h], pv[h]);
+                    if (VAR == 10)
+                        mn[q] = __hmin2(__hmin2(__hmin2(t[0], t[1]), __hmin2(t[2], t[3])), mn[q]);
+                    else
+                        mi[q] = vmin3(h2u(t[0]), h2u(t[1]), vmin3(h2u(t[2]), h2u(t[3]), mi[q]));
+                }
+            }
+            bool hit = false;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                if (VAR == 10) {
+                    const float2 m = __half22float2(mn[q]);
+                    hit |= fminf(m.x, m.y) <= thr[q];
+                } else {
+                    const int lo = (int)(short)(mi[q] & 0xffffu), hi = (int)(short)(mi[q] >> 16);
+                    hit |= (float)min(lo, hi) <= thr[q];
+                }
+            }
+            if (__any_sync(0xffffffffu, hit)) acc += 1.f;
+        }
+    }
+    unsigned long long c1 = clock64();
+    if (acc == 1234.5f) out[0] = acc;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *clk = Clk{c0, c1};
+}
+
 template <int Q, int G, int VAR>
 static void run(const char *name, int ctas_per_sm, const float *g, float *out, Clk *clk, int sms, double mhz_ref)
 {
-    auto k = (VAR >= 7) ? knn_loop_h2<Q, G, VAR> : VAR == 6 ? knn_loop_uni<Q, G, VAR> : knn_loop<Q, G, VAR>;
+    auto k = (VAR >= 10) ? knn_loop_h1<Q, G, VAR> : (VAR >= 7) ? knn_loop_h2<Q, G, VAR> : VAR == 6 ? knn_loop_uni<Q, G, VAR> : knn_loop<Q, G, VAR>;
     // pad the dynamic smem so at most ctas_per_sm CTAs fit on an SM
     size_t smem = 3 * TILE * sizeof(float);
     const size_t per = (227 * 1024) / ctas_per_sm;
@@ -304,6 +389,12 @@ int main()
         run<8, 32, 7>("fp16_hfma2_hmin2_q8", c, g, out, clk, sms, mhz);
         run<4, 32, 8>("fp16_hfma2_only_q4", c, g, out, clk, sms, mhz);
         run<4, 32, 9>("fp16_hfma2_hsetp2_q4", c, g, out, clk, sms, mhz);
+        run<4, 32, 10>("fp16_strip_hmin2_q4", c, g, out, clk, sms, mhz);
+        run<8, 32, 10>("fp16_strip_hmin2_q8", c, g, out, clk, sms, mhz);
+        run<4, 32, 11>("fp16_strip_vimnmx3_q4", c, g, out, clk, sms, mhz);
+        run<8, 32, 11>("fp16_strip_vimnmx3_q8", c, g, out, clk, sms, mhz);
+        run<4, 32, 12>("fp16_2d_vimnmx3_q4", c, g, out, clk, sms, mhz);
+        run<8, 32, 12>("fp16_2d_vimnmx3_q8", c, g, out, clk, sms, mhz);
     }
     return 0;
 }
