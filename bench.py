@@ -77,7 +77,9 @@ DFMA_PER_CLK_SM = 63.23  # measured (profiles/r01_pipe_peaks.json dfma_per_clk_s
 # table and a degree-3 polynomial (error 2^-36) 5, exponent 1, exp2 with a 64-entry table
 # and a degree-4 polynomial 8, two sums 2.
 DP_ALGO_PER_PAIR = 20
-KNN_FILTER_FMA_PER_PAIR = 2  # the kNN filter t = pp + a cx + b cy: one FFMA2 per pair
+KNN_FILTER_FMA_PER_PAIR = 2  # the r01 fp32 filter t = pp + a cx + b cy: 2 FMA per pair (one FFMA2 per couple)
+KNN_STRIP_FMA_PER_PAIR = 1   # round 2: the strip pre-test t1 = ps + A u, ONE fp16 FMA per pair (HFMA2: 2 per lane
+                             # per issue, the FFMA2 cadence) -- the least any exact brute-force pass can spend
 
 
 def weight_clk_per_pair(fp32=WEIGHT_FP32_PER_PAIR, transc=TRANSC_PER_PAIR):
@@ -671,14 +673,20 @@ def main():
 
 
 def knn_roofline(knn_ms, pairs, f_max, traffic=None):
-    """kNN filter kernel against its FMA-pipe bound: the expanded-form filter
-    t = pp + a cx + b cy needs 2 FMA lanes (one FFMA2) per pair."""
+    """kNN kernel against its FMA-pipe bound.  Since round 2 every pair is
+    touched by the strip pre-test t1 = ps + A u, one fp16 FMA per pair (HFMA2 carries two
+    per lane at the FFMA2 cadence), so the bound is ONE FMA per pair -- one arithmetic
+    operation per pair, the least an exact brute-force pass can do.  `frac_vs_fp32_filter`
+    keeps the round-1 bound (the fp32 filter's 2 FMA per pair) for comparison."""
     rate = pairs / (knn_ms / 1e3)
-    peak = N_SM * f_max * FMA_PER_CLK_SM / KNN_FILTER_FMA_PER_PAIR
+    peak = N_SM * f_max * FMA_PER_CLK_SM / KNN_STRIP_FMA_PER_PAIR
+    peak_r01 = N_SM * f_max * FMA_PER_CLK_SM / KNN_FILTER_FMA_PER_PAIR
     return {"kernel": "knn_filter_kernel (S1+S2 kNN pass)", "bound": "alu", "achieved": rate / 1e9,
             "peak": peak / 1e9, "unit": "Gpair/s", "frac": rate / peak, "traffic": traffic,
             "peak_basis": f"{N_SM} SM x {f_max / 1e6:.0f} MHz x {FMA_PER_CLK_SM} FMA lanes/clk / "
-                          f"{KNN_FILTER_FMA_PER_PAIR} FMA per pair (filter t = pp + a cx + b cy)"}
+                          f"{KNN_STRIP_FMA_PER_PAIR} FMA per pair (strip pre-test t1 = ps + A u, fp16, DESIGN.md 4.1)",
+            "frac_vs_fp32_filter": rate / peak_r01,
+            "fp32_filter_basis": f"{KNN_FILTER_FMA_PER_PAIR} FMA per pair (t = pp + a cx + b cy; the round-1 bound)"}
 
 
 def fp64_roofline(interp_ms, pairs, f_max, clocks):

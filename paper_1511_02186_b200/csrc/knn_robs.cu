@@ -487,9 +487,9 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
                 h16_convert<TILE>(spx + o, spy + o, hb, hb + TILE / 2, hb + TILE, hb + 3 * TILE / 2, axis, Cx, Cy,
                                   sig);
                 __syncthreads();
-                if (axis >= 0)
-                    knn_h16_tile<K, Q, G, TILE, true>(st, h16, hb, hb + TILE / 2, hb + TILE, hb + 3 * TILE / 2,
-                                                      scx + o, scy + o, spp + o, spx + o, spy + o, Cx, Cy, sig);
+                if (axis >= 0)  // strip groups of 4 G = 128 points (r02_tune_knn_strip_{d,e}.log)
+                    knn_h16_tile<K, Q, G, TILE, true, 4>(st, h16, hb, hb + TILE / 2, hb + TILE, hb + 3 * TILE / 2,
+                                                         scx + o, scy + o, spp + o, spx + o, spy + o, Cx, Cy, sig);
                 else
                     knn_h16_tile<K, Q, G, TILE, false>(st, h16, hb, hb + TILE / 2, hb + TILE, hb + 3 * TILE / 2,
                                                        scx + o, scy + o, spp + o, spx + o, spy + o, Cx, Cy, sig);
@@ -782,12 +782,10 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
     if (k <= 10) {  // large (spatially ordered) batches: Q = 4, G = 32 (108 vs 115 ms at C4)
         if (order_queries(a.nq) && a.nq >= 32768) {
             switch (knn_h16_mode()) {
-            case 1:  // Q = 2 below ~384K queries (strong-scaled shares), Q = 4 above; with the
-                     // strip pre-test (round 2) Q = 4 at 3 CTAs/SM (C4 59.4 ms; uncapped,
-                     // 193 registers: 64.9) and Q = 2 uncapped below (128,000 queries 9.0 ms)
-                     // -- profiles/r02_tune_knn_strip_a.log
-                if (a.nq < 393216) return launch_knn_filter_t<10, 2, 32, 0, float, true>(a, f, st, sp, fd);
-                return launch_knn_filter_t<10, 4, 32, 3, float, true>(a, f, st, sp, fd);
+            case 1:  // with the strip pre-test in 128-point groups (round 2) Q = 2 uncapped wins
+                     // at every size: C4 54.5 ms (Q = 4 at 3 CTAs/SM 58.0), 128,000 queries
+                     // 8.2, 32,768 3.4 -- profiles/r02_tune_knn_strip_d.log
+                return launch_knn_filter_t<10, 2, 32, 0, float, true>(a, f, st, sp, fd);
             case 3:  // the register-capped shapes (4 / 6 CTAs/SM), the round-2 default before the seeds
                 if (a.nq < 393216) return launch_knn_filter_t<10, 2, 32, 6, float, true>(a, f, st, sp, fd);
                 return launch_knn_filter_t<10, 4, 32, 4, float, true>(a, f, st, sp, fd);

@@ -432,7 +432,7 @@ __device__ __forceinline__ void h16_convert(const float *__restrict__ tpx, const
 // lane's strip test keeps runs the 2-D test, and only a group that passes both reaches
 // the rare path.  Both tests are necessary conditions of a true candidate, so the
 // selected multiset is unchanged.  !STRIP: the 2-D test alone (AIDW_KNN_STRIP=0).
-template <int K, int Q, int G, int TILE, bool STRIP>
+template <int K, int Q, int G, int TILE, bool STRIP, int SGM = 1>
 __device__ __forceinline__ void knn_h16_tile(KnnF32State<K, Q, float> &st, KnnH16<Q> &h, const __half2 *hu,
                                              const __half2 *hv, const __half2 *hp, const __half2 *hs,
                                              const float *__restrict__ tcx, const float *__restrict__ tcy,
@@ -471,20 +471,31 @@ __device__ __forceinline__ void knn_h16_tile(KnnF32State<K, Q, float> &st, KnnH1
         }
         return __any_sync(0xffffffffu, hit);
     };
+    auto rare = [&](int j, const bool (&hq)[Q]) {
+        knn_rare_group_impl<K, Q, G>(st, hq, tcx, tcy, tpp, tpx, tpy, j, [&](int q) {
+            h.T[q] = h16_threshold<STRIP>(st.buf[q][K - 1], st.qx[q], st.qy[q], Cx, Cy, sig, h.A[q], h.B[q]);
+        });
+    };
+    if constexpr (!STRIP) {
 #pragma unroll 1
-    for (int j = 0; j < TILE; j += G) {
-        bool hq[Q];
-        bool go;
-        if constexpr (!STRIP) {
+        for (int j = 0; j < TILE; j += G) {
+            bool hq[Q];
 #pragma unroll
             for (int q = 0; q < Q; ++q) hq[q] = true;
-            go = test2d(j, hq);
-        } else {
+            if (test2d(j, hq)) rare(j, hq);
+        }
+    } else {
+        // strip groups of SGM * G points per vote; a kept strip group runs the 2-D test per
+        // G-point group
+        constexpr int SG = SGM * G;
+        static_assert(TILE % SG == 0, "strip group size");
+#pragma unroll 1
+        for (int j = 0; j < TILE; j += SG) {
             __half2 mn[Q];
 #pragma unroll
             for (int q = 0; q < Q; ++q) mn[q] = __half2half2(__ushort_as_half((unsigned short)0x7c00));  // +inf
 #pragma unroll
-            for (int c = 0; c < G; c += 8) {
+            for (int c = 0; c < SG; c += 8) {
                 const uint32_t o = (uint32_t)(j + c) * 2u;
                 const float4 S4 = lds128(au + o), P4 = lds128(aps + o);
                 const __half2 *sv = reinterpret_cast<const __half2 *>(&S4);
@@ -497,19 +508,23 @@ __device__ __forceinline__ void knn_h16_tile(KnnF32State<K, Q, float> &st, KnnH1
                     mn[q] = __hmin2(__hmin2(__hmin2(t[0], t[1]), __hmin2(t[2], t[3])), mn[q]);
                 }
             }
-            bool hit = false;
+            bool hs1[Q], hit = false;
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
                 const float2 m = __half22float2(mn[q]);
-                hq[q] = fminf(m.x, m.y) <= h.T[q];
-                hit |= hq[q];
+                hs1[q] = fminf(m.x, m.y) <= h.T[q];
+                hit |= hs1[q];
             }
-            go = __any_sync(0xffffffffu, hit) && test2d(j, hq);
+            if (__any_sync(0xffffffffu, hit)) {
+#pragma unroll 1
+                for (int g = 0; g < SGM; ++g) {
+                    bool hq[Q];
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) hq[q] = hs1[q];
+                    if (test2d(j + g * G, hq)) rare(j + g * G, hq);
+                }
+            }
         }
-        if (go)
-            knn_rare_group_impl<K, Q, G>(st, hq, tcx, tcy, tpp, tpx, tpy, j, [&](int q) {
-                h.T[q] = h16_threshold<STRIP>(st.buf[q][K - 1], st.qx[q], st.qy[q], Cx, Cy, sig, h.A[q], h.B[q]);
-            });
     }
 }
 
