@@ -63,7 +63,6 @@ TRANSC_PER_PAIR = 2
 POLY_FMA_PER_TRANSC = 8
 MUFU_PER_CLK_SM = 15.96   # measured MUFU.EX2/LG2 per SM per clock
 FMA_PER_CLK_SM = 123.2    # measured FFMA2 (packed) FMA ops per SM per clock
-KNN_FP32_PER_PAIR = 4     # canonical kNN distance (2 sub, mul, fma) -- SIMT FP32 bound
 N_SM = 148
 # fp64 (--dtype f64): the weighting pass has no hardware transcendental;
 # per pair the kernel issues 21 FP64 operations (round 2: distance 4, table + degree-3
@@ -586,7 +585,7 @@ def main():
           {"general": 1.0, "a1": 0.0, "a2": 0.0, "a3": 0.0})
     w_clk = weight_clk_mix(fr)
     sfu_peak_pairs = N_SM * f_max / w_clk
-    path_clk_per_pair = KNN_FP32_PER_PAIR / FMA_PER_CLK_SM + w_clk
+    path_clk_per_pair = KNN_STRIP_FMA_PER_PAIR / FMA_PER_CLK_SM + w_clk
     path_peak_pairs = N_SM * f_max / path_clk_per_pair
     traffic = knn_traffic = None
     try:
@@ -602,7 +601,7 @@ def main():
         roof = {"bound": "alu", "kernel": "fused_fixed_kernel (N1: S1..S5 in one launch)",
                 "achieved": fused_rate / 1e9, "peak": path_peak_pairs / 1e9, "unit": "Gpair/s",
                 "frac": fused_rate / path_peak_pairs, "traffic": None,
-                "peak_basis": "kNN 4 FP32/pair on the FMA pipe + the pipe-balanced weighting bound "
+                "peak_basis": "kNN 1 FMA/pair (the strip pre-test) on the FMA pipe + the pipe-balanced weighting bound "
                               f"({w_clk:.4f} clk/pair), {N_SM} SM x {f_max / 1e6:.0f} MHz"}
         phases = {"fused": knn_ms}
     elif f64:
@@ -622,7 +621,8 @@ def main():
             "general_clk_per_pair": weight_clk_per_pair(),
             "sfu_only_peak": N_SM * MUFU_PER_CLK_SM / TRANSC_PER_PAIR * f_max / 1e9,
             "path_frac": (pairs / (ms / 1e3)) / path_peak_pairs,
-            "path_peak_basis": "kNN 4 FP32/pair on the FMA pipe + the weighting bound above, per SM",
+            "path_peak_basis": "kNN 1 FMA/pair (the strip pre-test, DESIGN.md 4.1) on the FMA pipe + the weighting "
+                               "bound above, per SM",
             "frac_at_measured_clock": (interp_rate / sfu_peak_pairs) * (f_max / (clocks["sm_mhz"] * 1e6))
             if clocks.get("sm_mhz") else None,
             "knn": knn_roofline(knn_ms, pairs, f_max, knn_traffic),
