@@ -316,14 +316,15 @@ template <typename T> __host__ __device__ constexpr int filter_arrays() { return
 
 // SPLIT: 0 = whole data range; 1 = a split (seeded from the home tile when the batch is
 // spatially ordered); 2 = an unordered split with the per-query seed (seed_query).
-// H16: fp32 handles, spatially ordered batches -- the fp16 pre-filter (passes.cuh
-// knn_h16_tile) replaces the fp32 main loop once every query of the CTA has a finite
-// k-th distance (after the seed tile, or the first tile).
+// H16: spatially ordered batches -- the fp16 pre-filter (passes.cuh knn_h16_tile)
+// replaces the fp32 main loop once every query of the CTA has a finite k-th distance
+// (after the seed tile, or the first tile).  fp32 handles convert the tile's coordinates;
+// fp64 handles (round 2) convert the centred fp32 filter coordinates cx = fl32(x - c), the
+// CTA centre taken on the same centred scale, with the centring error in the margin.
 template <typename T, int K, int Q, int G, int SPLIT, int MINB = 0, bool H16 = false>
 __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<T> a, const FilterArgs f)
 {
     constexpr int TILE = kTileKF, STAGES = kStagesKF, NARR = filter_arrays<T>();
-    static_assert(!H16 || NARR == 5, "the fp16 pre-filter is for fp32 handles");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float *scx = reinterpret_cast<float *>(smem_raw);
     float *scy = scx + STAGES * TILE;
@@ -352,8 +353,8 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
         home = home >= nt_all ? nt_all - 1 : home;
     }
     // H16 kernels seed every query's lists from its own Morton cell instead (per-query seed,
-    // f.sx != null): no home tile to scan, and the fp16 loop starts on the first tile
-    const bool qseed = H16 && a.perm != nullptr && f.sx != nullptr;
+    // f.sx / f.sx64 != null): no home tile to scan, and the fp16 loop starts on the first tile
+    const bool qseed = H16 && a.perm != nullptr && (NARR == 5 ? f.sx != nullptr : f.sx64 != nullptr);
     const bool seed = SPLIT && a.perm != nullptr && !qseed;
     int start = 0;
     if (!SPLIT && a.perm) start = home == 0 ? nt_all - 1 : home - 1;
@@ -409,8 +410,10 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
     // coefficients and thresholds; enabled once every query has a finite k-th distance
     __shared__ __align__(16) __half2 hbuf[H16 ? 2 : 1][4][H16 ? TILE / 2 : 1];
     __shared__ unsigned hred[4];
+    __shared__ H16Frame hfr;
     KnnH16<Q> h16;
-    float Cx = 0.f, Cy = 0.f, sig = 0.f;
+    float Cx = 0.f, Cy = 0.f, sig = 0.f;  // fp64 handles: C on the centred (cx, cy) scale
+    float hq_x[H16 ? Q : 1], hq_y[H16 ? Q : 1];  // the queries on the scale of the converted points
     bool h16_on = false;
     int axis = -1;  // strip axis: the one along which the CTA's queries spread least
     if constexpr (H16) {
@@ -418,14 +421,19 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
         auto key = [](float v) { const unsigned b = __float_as_uint(v); return (b >> 31) ? ~b : b | 0x80000000u; };
         auto unkey = [](unsigned k) { return __uint_as_float((k >> 31) ? k & 0x7fffffffu : ~k); };
         if (threadIdx.x == 0) hred[0] = hred[2] = 0xffffffffu, hred[1] = hred[3] = 0u;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            hq_x[q] = NARR == 5 ? (float)qx[q] : centre_f32(qx[q], f.c_x);
+            hq_y[q] = NARR == 5 ? (float)qy[q] : centre_f32(qy[q], f.c_y);
+        }
         __syncthreads();
 #pragma unroll
         for (int q = 0; q < Q; ++q)
-            if (valid[q] && isfinite(qx[q]) && isfinite(qy[q])) {
-                atomicMin(&hred[0], key(qx[q]));
-                atomicMax(&hred[1], key(qx[q]));
-                atomicMin(&hred[2], key(qy[q]));
-                atomicMax(&hred[3], key(qy[q]));
+            if (valid[q] && isfinite(hq_x[q]) && isfinite(hq_y[q])) {
+                atomicMin(&hred[0], key(hq_x[q]));
+                atomicMax(&hred[1], key(hq_x[q]));
+                atomicMin(&hred[2], key(hq_y[q]));
+                atomicMax(&hred[3], key(hq_y[q]));
             }
         __syncthreads();
         if (hred[0] != 0xffffffffu) {
@@ -442,13 +450,13 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
     auto h16_enable = [&]() -> bool {
         bool fin = true;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) fin &= !valid[q] || st.buf[q][K - 1] < pos_inf<float>();
+        for (int q = 0; q < Q; ++q) fin &= !valid[q] || st.buf[q][K - 1] < pos_inf<T>();
         if (!__syncthreads_and(fin)) return false;
         float m = 0.f;  // non-negative: float bits order like uint
 #pragma unroll
         for (int q = 0; q < Q; ++q)
             if (valid[q]) {
-                const float dx = qx[q] - Cx, dy = qy[q] - Cy;
+                const float dx = hq_x[q] - Cx, dy = hq_y[q] - Cy;
                 m = fmaxf(m, fmaxf(sqrtf(dx * dx + dy * dy), sqrtf((float)st.buf[q][K - 1])));
             }
         if (threadIdx.x == 0) hred[0] = 0u;
@@ -462,15 +470,23 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
         sig = ldexpf(1.0f, e);
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            const float ax = -2.0f * __fmul_rn(__fsub_rn(qx[q], Cx), sig);
-            const float by = -2.0f * __fmul_rn(__fsub_rn(qy[q], Cy), sig);
+            const float ax = -2.0f * __fmul_rn(__fsub_rn(hq_x[q], Cx), sig);
+            const float by = -2.0f * __fmul_rn(__fsub_rn(hq_y[q], Cy), sig);
             // the strip axis' coefficient goes first (h16_convert swaps û, v̂ likewise)
             h16.A[q] = __float2half2_rn(axis == 1 ? by : ax);
             h16.B[q] = __float2half2_rn(axis == 1 ? ax : by);
-            const float v = st.buf[q][K - 1];
+        }
+        if (threadIdx.x == 0) {
+            const double ox = NARR == 5 ? 0.0 : (double)f.c_x, oy = NARR == 5 ? 0.0 : (double)f.c_y;
+            hfr = H16Frame{ox + (double)Cx, oy + (double)Cy, ox, oy, NARR == 5 ? 0.0 : (double)f.r1, sig, NARR != 5};
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const T v = st.buf[q][K - 1];
             h16.T[q] = !valid[q] ? -pos_inf<float>()
-                       : axis < 0 ? h16_threshold<false>(v, qx[q], qy[q], Cx, Cy, sig, h16.A[q], h16.B[q])
-                                  : h16_threshold<true>(v, qx[q], qy[q], Cx, Cy, sig, h16.A[q], h16.B[q]);
+                       : axis < 0 ? h16_threshold<false>(v, qx[q], qy[q], hfr, h16.A[q], h16.B[q])
+                                  : h16_threshold<true>(v, qx[q], qy[q], hfr, h16.A[q], h16.B[q]);
         }
         return isfinite(mm) && sig > 0.f && isfinite(sig);
     };
@@ -484,24 +500,42 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
         if constexpr (H16) {
             if (h16_on) {
                 __half2 *hb = &hbuf[t & 1][0][0];
-                h16_convert<TILE>(spx + o, spy + o, hb, hb + TILE / 2, hb + TILE, hb + 3 * TILE / 2, axis, Cx, Cy,
-                                  sig);
+                // fp32: the tile's coordinates; fp64: the centred filter coordinates
+                h16_convert<TILE>(NARR == 5 ? spx + o : scx + o, NARR == 5 ? spy + o : scy + o, hb, hb + TILE / 2,
+                                  hb + TILE, hb + 3 * TILE / 2, axis, Cx, Cy, sig);
                 __syncthreads();
+                const T *rpx, *rpy;  // the canonical re-check's coordinates (rare path)
+                if constexpr (NARR == 5) {
+                    rpx = spx + o;
+                    rpy = spy + o;
+                } else {
+                    const int64_t off = (int64_t)tile_of(t) * TILE;
+                    rpx = f.px64 + off;
+                    rpy = f.py64 + off;
+                }
                 if (axis >= 0)  // strip groups of 4 G = 128 points (r02_tune_knn_strip_{d,e}.log)
-                    knn_h16_tile<K, Q, G, TILE, true, 4>(st, h16, hb, hb + TILE / 2, hb + TILE, hb + 3 * TILE / 2,
-                                                         scx + o, scy + o, spp + o, spx + o, spy + o, Cx, Cy, sig);
+                    knn_h16_tile<K, Q, G, TILE, true, 4, T>(st, h16, hb, hb + TILE / 2, hb + TILE, hb + 3 * TILE / 2,
+                                                            scx + o, scy + o, spp + o, rpx, rpy, hfr);
                 else
-                    knn_h16_tile<K, Q, G, TILE, false>(st, h16, hb, hb + TILE / 2, hb + TILE, hb + 3 * TILE / 2,
-                                                       scx + o, scy + o, spp + o, spx + o, spy + o, Cx, Cy, sig);
+                    knn_h16_tile<K, Q, G, TILE, false, 1, T>(st, h16, hb, hb + TILE / 2, hb + TILE,
+                                                             hb + 3 * TILE / 2, scx + o, scy + o, spp + o, rpx, rpy,
+                                                             hfr);
             } else {  // warm-up tile (lists not yet finite): every group straight to the rare
                       // path -- with an infinite threshold the filter passes every pair anyway --
                       // so the kernel carries no fp32 main loop (registers)
                 bool all[Q];
 #pragma unroll
                 for (int q = 0; q < Q; ++q) all[q] = true;
+                if constexpr (NARR == 5) {
 #pragma unroll 1
-                for (int j = 0; j < TILE; j += G)
-                    knn_rare_group<K, Q, G>(st, all, scx + o, scy + o, spp + o, spx + o, spy + o, j);
+                    for (int j = 0; j < TILE; j += G)
+                        knn_rare_group<K, Q, G>(st, all, scx + o, scy + o, spp + o, spx + o, spy + o, j);
+                } else {
+                    const int64_t off = (int64_t)tile_of(t) * TILE;
+#pragma unroll 1
+                    for (int j = 0; j < TILE; j += G)
+                        knn_rare_group<K, Q, G>(st, all, scx + o, scy + o, spp + o, f.px64 + off, f.py64 + off, j);
+                }
             }
         } else if constexpr (NARR == 5) {
             knn_f32_tile<K, Q, G, TILE>(st, scx + o, scy + o, spp + o, spx + o, spy + o);
@@ -675,13 +709,17 @@ static int launch_knn_filter_t(KnnArgs<T> a, const FilterArgs &f, cudaStream_t s
             fo.pp = c + 5 * a.ndp;
             fo.px = c + 6 * a.ndp;
             fo.py = c + 7 * a.ndp;
-            if (H16 && knn_qseed_enabled()) {  // per-query seeds from the sorted copy
+            if (H16 && knn_qseed_enabled() && sizeof(T) == 4) {  // per-query seeds from the sorted copy
                 fo.sx = fo.px;
                 fo.sy = fo.py;
             }
             if (fd->coords64) {  // fp64 handles: the sorted fp64 coordinates for the re-check
                 fo.px64 = fd->coords64;
                 fo.py64 = fd->coords64 + a.ndp;
+                if (H16 && knn_qseed_enabled()) {  // and for the per-query seeds
+                    fo.sx64 = fo.px64;
+                    fo.sy64 = fo.py64;
+                }
             }
         }
     }
@@ -735,7 +773,11 @@ static int dispatch_filter_k(const KnnArgs<double> &a, const FilterArgs &f, cuda
     if (k <= 2) return launch_knn_filter_t<2, 2, 16, 0, double>(a, f, st, sp, fd);
     if (k <= 4) return launch_knn_filter_t<4, 2, 16, 0, double>(a, f, st, sp, fd);
     if (k <= 8) return launch_knn_filter_t<8, 2, 16, 0, double>(a, f, st, sp, fd);
-    if (k <= 10) return launch_knn_filter_t<10, 2, 16, 0, double>(a, f, st, sp, fd);
+    if (k <= 10) {  // spatially ordered batches: the fp16 pre-filter with the strip test (round 2)
+        if (fd && fd->cell_start && order_queries(a.nq) && a.nq >= 32768 && knn_h16_mode() != 0)
+            return launch_knn_filter_t<10, 2, 32, 0, double, true>(a, f, st, sp, fd);
+        return launch_knn_filter_t<10, 2, 16, 0, double>(a, f, st, sp, fd);
+    }
     if (k <= 12) return launch_knn_filter_t<12, 2, 16, 0, double>(a, f, st, sp, fd);
     if (k <= 15) return launch_knn_filter_t<15, 2, 16, 0, double>(a, f, st, sp, fd);
     if (k <= 16) return launch_knn_filter_t<16, 2, 16, 0, double>(a, f, st, sp, fd);

@@ -365,23 +365,40 @@ constexpr float kH16Clamp = 256.0f, kH16PPClamp = 32768.0f, kH16Radius = 16.0f;
 // 2-D bound dominates its one-axis counterpart, so the same formula with |q̂|² replaced by
 // the strip axis' share â² (A is the strip axis' coefficient) bounds t̂1.  The 2-D
 // threshold is T1 - b̂², rounded up (h16_t2d).  !STRIP: the 2-D threshold itself.
-template <bool STRIP>
-__device__ __forceinline__ float h16_threshold(float v, float qx, float qy, float Cx, float Cy, float sig,
-                                               __half2 A, __half2 B)
+// The CTA's fp16 frame (CTA-uniform, kept in shared memory: only the rare path reads it).
+// The converted points are fl16(sigma (p' - C)) with p' the tile's coordinates: the data
+// coordinates themselves (fp32 handles, o = 0) or the centred filter coordinates
+// cx = fl32(x - c) of fp64 handles (o = c, `centred`).  In the latter each converted
+// coordinate (point and query alike) carries the centring rounding, <= 2^-24 |x - c| per
+// axis, so the displacement bound Delta grows by sigma 2^-23 (r1 + |q - c|_1) (r1 >= the
+// data's largest |x - c|_1; factor 2 of slack).
+struct H16Frame {
+    double Cx, Cy;  // C in the data's coordinates (o + the centre on the converted scale)
+    double ox, oy;  // o
+    double r1;      // centred: r1; else 0
+    float sig;
+    int centred;
+};
+
+template <bool STRIP, typename T>
+__device__ __forceinline__ float h16_threshold(T v, T qx, T qy, const H16Frame &fr, __half2 A, __half2 B)
 {
-    if (!(v < pos_inf<float>())) return pos_inf<float>();
+    if (!(v < pos_inf<T>())) return pos_inf<float>();
     const double u16 = 0x1p-11, up = 0x1p-11 + 0x1p-22;
-    const double dx = (double)qx - (double)Cx, dy = (double)qy - (double)Cy;
-    const double Qn = (double)sig * sqrt(dx * dx + dy * dy) * (1.0 + 0x1p-40);
-    const double r = (double)sig * sqrt((double)v * (1.0 + 0x1p-20));
+    const double sig = (double)fr.sig;
+    const double dx = (double)qx - fr.Cx, dy = (double)qy - fr.Cy;
+    const double Qn = sig * sqrt(dx * dx + dy * dy) * (1.0 + 0x1p-40);
+    const double r = sig * sqrt((double)v * (1.0 + 0x1p-20));
     const double ah = 0.5 * (double)__low2float(A), bh = 0.5 * (double)__low2float(B);
     const double qq = ah * ah + bh * bh;  // |q̂|², exact
     const double Qb = fmax(Qn, sqrt(qq)) * (1.0 + up);
-    const double D = up * (2.0 * Qb + r);
+    const double ce = fr.centred ? sig * 0x1p-23 * (fr.r1 + fabs((double)qx - fr.ox) + fabs((double)qy - fr.oy)) * 1.001
+                                 : 0.0;
+    const double D = up * (2.0 * Qb + r) + ce;
     const double P = Qb + r + D, R = r + D;
-    const double T = R * R - (STRIP ? ah * ah : qq) + up * P * P + 1.002 * u16 * (P * P + Qb * Qb + R * R) +
-                     0x1p-18;
-    return __double2float_ru(T);
+    const double th = R * R - (STRIP ? ah * ah : qq) + up * P * P + 1.002 * u16 * (P * P + Qb * Qb + R * R) +
+                      0x1p-18;
+    return __double2float_ru(th);
 }
 
 // The 2-D test's threshold from the strip threshold T1: T1 - (B/2)², the product exact in
@@ -432,12 +449,12 @@ __device__ __forceinline__ void h16_convert(const float *__restrict__ tpx, const
 // lane's strip test keeps runs the 2-D test, and only a group that passes both reaches
 // the rare path.  Both tests are necessary conditions of a true candidate, so the
 // selected multiset is unchanged.  !STRIP: the 2-D test alone (AIDW_KNN_STRIP=0).
-template <int K, int Q, int G, int TILE, bool STRIP, int SGM = 1>
-__device__ __forceinline__ void knn_h16_tile(KnnF32State<K, Q, float> &st, KnnH16<Q> &h, const __half2 *hu,
+template <int K, int Q, int G, int TILE, bool STRIP, int SGM = 1, typename T = float>
+__device__ __forceinline__ void knn_h16_tile(KnnF32State<K, Q, T> &st, KnnH16<Q> &h, const __half2 *hu,
                                              const __half2 *hv, const __half2 *hp, const __half2 *hs,
                                              const float *__restrict__ tcx, const float *__restrict__ tcy,
-                                             const float *__restrict__ tpp, const float *__restrict__ tpx,
-                                             const float *__restrict__ tpy, float Cx, float Cy, float sig)
+                                             const float *__restrict__ tpp, const T *__restrict__ tpx,
+                                             const T *__restrict__ tpy, const H16Frame &fr)
 {
     static_assert(G % 8 == 0 && G <= 32 && TILE % G == 0, "group size");
     const uint32_t au = smem_addr(hu), av = smem_addr(hv), ap = smem_addr(hp), aps = smem_addr(hs);
@@ -473,7 +490,7 @@ __device__ __forceinline__ void knn_h16_tile(KnnF32State<K, Q, float> &st, KnnH1
     };
     auto rare = [&](int j, const bool (&hq)[Q]) {
         knn_rare_group_impl<K, Q, G>(st, hq, tcx, tcy, tpp, tpx, tpy, j, [&](int q) {
-            h.T[q] = h16_threshold<STRIP>(st.buf[q][K - 1], st.qx[q], st.qy[q], Cx, Cy, sig, h.A[q], h.B[q]);
+            h.T[q] = h16_threshold<STRIP>(st.buf[q][K - 1], st.qx[q], st.qy[q], fr, h.A[q], h.B[q]);
         });
     };
     if constexpr (!STRIP) {

@@ -772,8 +772,47 @@ def test_knn_filter_translated_scaled(P, orc, offset, scale):
     assert rel_err(Zg, Zo).max() <= 1e-4
 
 
+@pytest.mark.parametrize("case", ["uniform", "clustered", "offset", "scaled", "outliers"])
+def test_knn_h16_f64_bit_identical(P, orc, monkeypatch, case):
+    """fp64 handles with the fp16 pre-filter and strip test (round 2; the converted points
+    are the centred fp32 filter coordinates, the centring rounding in the margin,
+    passes.cuh H16Frame): on off-grid fp64 inputs -- uniform, clustered, translated by
+    10^6 (fp32 ulp 0.06 before centring), scaled by 10^12, with duplicates, coincident
+    and far-outside queries -- lists, r_obs, d1^2 and bounds are bit-identical to the
+    fp32-filter kernel (AIDW_KNN_H16=0) and bit-exact against the fp64 oracle on a sample."""
+    rng = np.random.default_rng(606)
+    nq = 60000
+    if case == "clustered":
+        x, y, z = datagen.make_data({"nd": 50000, "data": "clustered"}, seed=79)
+        x, y = x + rng.random(len(x)) * 2.0 ** -30, y + rng.random(len(y)) * 2.0 ** -30  # off the grid
+    else:
+        x, y = rng.random(50000), rng.random(50000)
+        z = 1.0 + rng.random(50000)
+    qx, qy = rng.random(nq), rng.random(nq)
+    if case == "offset":
+        x, y, qx, qy = 1.0e6 + x, 1.0e6 + y, 1.0e6 + qx, 1.0e6 + qy
+    if case == "scaled":
+        x, y, qx, qy = x * 1.0e12, y * 1.0e12, qx * 1.0e12, qy * 1.0e12
+    if case == "outliers":
+        x[1::7], y[1::7] = x[::7][: len(x[1::7])], y[::7][: len(y[1::7])]  # duplicates
+        qx[::13], qy[::13] = x[: len(qx[::13])], y[: len(qy[::13])]       # coincident
+        qx[::501] = qx[::501] * 50.0 - 20.0                               # far outside
+    res = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("AIDW_KNN_H16", flag)
+        eng = P.AIDW(x, y, z, dtype=torch.float64)
+        res[flag] = gpu_knn(P, eng, qx, qy, 10)
+        eng.close()
+    for u, v in zip(res["0"], res["1"]):
+        assert np.array_equal(u, v)
+    sub = np.arange(0, nq, 197)
+    ro, do = orc.knn_f64(x, y, qx[sub], qy[sub], 10, want_dists=True)
+    assert np.array_equal(res["1"][3][sub], do) and np.array_equal(res["1"][0][sub], ro)
+
+
 @pytest.mark.parametrize("offset,scale,nq", [(0.0, 1.0, 900), (1.0e6, 1.0e-3, 900), (-3.0e4, 1.0e12, 900),
-                                             (0.25, 2.0 ** -50, 900), (0.0, 2.0 ** -70, 900), (7.0, 1.0, 40000)])
+                                             (0.25, 2.0 ** -50, 900), (0.0, 2.0 ** -70, 900), (7.0, 1.0, 40000),
+                                             (1.0e6, 1.0e-3, 40000), (-3.0e4, 1.0e12, 40000)])
 def test_knn_filter_f64(P, orc, monkeypatch, offset, scale, nq):
     """fp64 handles share the fp32 filter with an fp64 canonical re-check:
     on fp64 inputs that fp32 cannot represent, translated and scaled (2^-70: the data

@@ -188,3 +188,87 @@ def test_strip_mutation_detected():
         u, _, _ = convert(fl32(qx + rad * rng.choice([-1.0, 1.0])), qy, cx, cy, sig)
         lost += fma16(a, u, strip_convert(u)) > bare
     assert lost > 0
+
+
+# ---------------------------------------------------------------------------------
+# fp64 handles (round 2): the converted points are the centred fp32 filter coordinates
+# cx = fl32(x - c) (c the fp32 data-bbox centre), the CTA centre C lives on the same
+# centred scale, and the threshold adds the centring term of passes.cuh H16Frame:
+# sigma 2^-23 (r1 + |q - c|_1) to the displacement bound.
+
+def threshold_frame(v, qx, qy, Cxd, Cyd, ox, oy, r1, sig, a, b, strip, centred=True):
+    """h16_threshold<STRIP, double> (passes.cuh), restated."""
+    if not v < math.inf:
+        return math.inf
+    dx, dy = qx - Cxd, qy - Cyd
+    qn = sig * math.sqrt(dx * dx + dy * dy) * (1.0 + 2.0 ** -40)
+    r = sig * math.sqrt(v * (1.0 + 2.0 ** -20))
+    ah, bh = 0.5 * a, 0.5 * b
+    qq = ah * ah + bh * bh
+    qb = max(qn, math.sqrt(qq)) * (1.0 + UP)
+    ce = sig * 2.0 ** -23 * (r1 + abs(qx - ox) + abs(qy - oy)) * 1.001 if centred else 0.0
+    d = UP * (2.0 * qb + r) + ce
+    p = qb + r + d
+    rr = r + d
+    t = rr * rr - (ah * ah if strip else qq) + UP * p * p + 1.002 * U16 * (p * p + qb * qb + rr * rr) + 2.0 ** -18
+    return ru32(t)
+
+
+def canon64(qx, qy, px, py):
+    """The fp64 canonical s = fma(dx, dx, dy*dy) (R16): one rounding of the exact value
+    (int / int true division in Python rounds correctly)."""
+    dx, dy = qx - px, qy - py
+    ex = Fraction(dx) * Fraction(dx) + Fraction(dy * dy)
+    return ex.numerator / ex.denominator
+
+
+def check_case_f64(rng, region, kth, centred=True, n_q=30, n_p=50):
+    """Data spread over [0, 1)^2 (r1 ~ 1), a CTA region of half-width `region` somewhere
+    inside, k-th distances ~kth: the centring rounding (~2^-25 absolute) is then a
+    sizeable share of the scaled margin when region and kth are small."""
+    c_x, c_y = fl32(0.5 + 2.0 ** -30 * 3), fl32(0.5 - 2.0 ** -31 * 5)
+    r1 = float(f32((0.5 + 0.5) * (1.0 + 1e-6)))
+    ctr = (rng.uniform(0.1, 0.9), rng.uniform(0.1, 0.9))
+    qs = [(ctr[0] + rng.uniform(-1, 1) * region, ctr[1] + rng.uniform(-1, 1) * region) for _ in range(n_q)]
+    hq = [(fl32(qx - c_x), fl32(qy - c_y)) for qx, qy in qs]
+    C = (fl32(0.5 * min(h[0] for h in hq)) + fl32(0.5 * max(h[0] for h in hq)),
+         fl32(0.5 * min(h[1] for h in hq)) + fl32(0.5 * max(h[1] for h in hq)))
+    C = (fl32(C[0]), fl32(C[1]))
+    vs = [(kth * rng.uniform(0.5, 1.5)) ** 2 for _ in qs]
+    m = max(max(math.hypot(h[0] - C[0], h[1] - C[1]), math.sqrt(v)) for h, v in zip(hq, vs)) * 1.001
+    sig = 2.0 ** (math.frexp(16.0 / m)[1] - 1)
+    lost = 0
+    for (qx, qy), (hx, hy), v in zip(qs, hq, vs):
+        a, b = coeffs(hx, hy, C[0], C[1], sig)
+        for _ in range(n_p):
+            ang = rng.choice([0.0, 0.5 * math.pi, math.pi, 1.5 * math.pi]) if rng.uniform() < 0.3 else rng.uniform(0, 2 * math.pi)
+            rad = math.sqrt(v) * (1.0 - 10 ** rng.uniform(-9, -0.3))
+            px, py = qx + rad * math.cos(ang), qy + rad * math.sin(ang)
+            if not canon64(qx, qy, px, py) < v:
+                continue
+            cx, cy = fl32(px - c_x), fl32(py - c_y)
+            u, w, pp = convert(cx, cy, C[0], C[1], sig)
+            for (c1, s1, c2, s2) in ((a, u, b, w), (b, w, a, u)):
+                T1 = threshold_frame(v, qx, qy, c_x + C[0], c_y + C[1], c_x, c_y, r1, sig, c1, c2, True, centred)
+                t1 = fma16(c1, s1, strip_convert(s1))
+                pp2 = fl16(min(fma32(s1, s1, fl32(s2 * s2)), 32768.0))
+                t2 = fma16(c2, s2, fma16(c1, s1, pp2))
+                ok = t1 <= T1 and t2 <= t2d(T1, c2)
+                if centred:
+                    assert ok, (qx, qy, px, py, v, t1, T1)
+                lost += not ok
+    return lost
+
+
+def test_h16_margin_f64_centred_keeps_every_candidate():
+    rng = np.random.default_rng(2025)
+    for region, kth in ((1e-2, 2e-3), (2.0 ** -14, 2.0 ** -17), (2.0 ** -18, 2.0 ** -20), (1e-6, 3e-7), (1e-7, 2e-8)):
+        for _ in range(6):
+            check_case_f64(rng, region, kth)
+
+
+def test_h16_margin_f64_centring_term_needed():
+    """Mutation check: without the centring term the fp64 thresholds lose true candidates
+    once the CTA region is small against the data extent."""
+    rng = np.random.default_rng(5)
+    assert check_case_f64(rng, 1e-6, 3e-7, centred=False, n_q=10, n_p=40) > 0

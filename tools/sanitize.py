@@ -46,9 +46,13 @@ for dt in (torch.float32, torch.float64):
     eng.run(qx, qy, 10, LV, P.GLOBAL)
     eng.run(bx, by, 10, LV, P.GLOBAL)  # unsplit ordered batch (fp16 pre-filter from tile 1)
     del os.environ["AIDW_SPLIT"]
-    os.environ["AIDW_KNN_H16"] = "2"  # the uncapped fp16 pre-filter kernel
+    os.environ["AIDW_KNN_H16"] = "2"  # the Q = 4 fp16 pre-filter kernel
     eng.run(bx, by, 10, LV, P.GLOBAL)
     del os.environ["AIDW_KNN_H16"]
+    eng.run(bx, by, 15, LV, P.GLOBAL)  # k = 15 ordered: the fp16 kernel with the strip test
+    os.environ["AIDW_KNN_STRIP"] = "0"  # the fp16 kernels without the strip pre-test
+    eng.run(bx, by, 10, LV, P.GLOBAL)
+    del os.environ["AIDW_KNN_STRIP"]
     # device-side bounds exchange with one rank (push, wait, acks)
     eng.exchange_connect([eng.exchange_setup(0, 1)])
     for _ in range(3):
