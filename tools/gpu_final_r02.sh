@@ -1,7 +1,8 @@
 # Round-2 final evidence (run under gpurun from the repo root): bash tools/gpu_final_r02.sh TAG
 # build + smoke, pytest -m gpu (C4 + C5 golden), the default bench line, C5 strong N = 1,
 # a 2-rank gloo logic run of the default bench (ranks share the GPU), the reference
-# (oracle) arm, the ncu launch list of the bench step, the Table-1 ablation.
+# (oracle) arm, the ncu launch list of the bench step, ncu captures of the kNN and the
+# weighting kernel, the C4 strong-scaling shares, the Table-1 ablation.
 cd "${GRAFT_REPO_ROOT:-.}"
 TAG=${1:-r02final}
 O=gpurun_out/$TAG
@@ -19,5 +20,13 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:"knn
 python tools/ncu_summary.py $O/prof_knn.ncu-rep --json $O/ncu_knn_summary.json > /dev/null 2>&1
 XM=sm__inst_executed_pipe_xu.sum,sm__inst_executed_pipe_fmaheavy.sum,sm__inst_executed_pipe_fmalite.sum,sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fmalite_cycles_active.avg.pct_of_peak_sustained_active,sm__cycles_active.avg,sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active,gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 timeout 600 ncu --metrics $XM --clock-control none -k regex:"interp_f32x2|knn_filter" -c 2 --csv --page raw python bench.py --profile --warmup 0 > $O/ncu_xu.csv 2> $O/ncu_xu.err
+# strong-scaling shares of C4: each rank's block (1,024,000 / P queries) timed alone
+for share in 512000 256000 128000; do
+  timeout 600 python bench.py --nq $share --no-f64 --no-cpu-baseline --no-e2e > $O/share_$share.json 2>> $O/bench.err
+done
+python tools/strong_shares.py $O/bench.json $O/share_512000.json $O/share_256000.json $O/share_128000.json \
+    > $O/strong_shares.json 2>> $O/bench.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"interp_f32x2" -c 1 -o $O/prof_interp python bench.py --profile --warmup 0 > $O/ncu_interp.log 2>&1
+python tools/ncu_summary.py $O/prof_interp.ncu-rep --json $O/ncu_interp_summary.json > /dev/null 2>&1
 timeout 1200 python tools/table1.py --out $O/table1.md --json $O/table1.jsonl > $O/table1.log 2>&1
 echo done

@@ -1,6 +1,7 @@
 # Round-2 measurement sweeps (run under gpurun from the repo root):
 #   bash tools/gpu_sweeps.sh strip TAG       kNN strip pre-test: shapes (AIDW_KNN_VARIANT) and
 #                                            strip on/off (AIDW_KNN_STRIP) at C4 sizes, C3, C5
+#   bash tools/gpu_sweeps.sh ksplit TAG      kNN seeded split factor (AIDW_SPLIT) at C4 and the shares
 #   bash tools/gpu_sweeps.sh tail TAG        weighting pass: wave quantisation (time per query
 #                                            at grids of 32.0 .. 48.05 waves)
 #   bash tools/gpu_sweeps.sh ncu_interp TAG  ncu --set full of the weighting kernel + its
@@ -20,6 +21,14 @@ strip)
     timeout 300 env TUNE_CFG=$c AIDW_KNN_STRIP=0 python tools/tune_knn.py | sed 's/^/strip0 /' >> $O/tune.log 2>&1
   done
   timeout 900 python -m pytest tests -m gpu -q -k "h16 or golden or knn" > $O/pytest.log 2>&1; echo rc=$? >> $O/pytest.log
+  ;;
+ksplit)
+  for nq in 1024000 512000 128000; do
+    for sp in auto 0 2 3 4 5 6 8; do
+      if [ $sp = auto ]; then timeout 300 python tools/tune_knn.py $nq >> $O/tune.log 2>&1
+      else timeout 300 env AIDW_SPLIT=$sp python tools/tune_knn.py $nq >> $O/tune.log 2>&1; fi
+    done
+  done
   ;;
 tail)
   for nq in 1024000 1022976 1017856 1011712 1000000 989184 682240 681984; do
