@@ -29,4 +29,5 @@ python tools/strong_shares.py $O/bench.json $O/share_512000.json $O/share_256000
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"interp_f32x2" -c 1 -o $O/prof_interp python bench.py --profile --warmup 0 > $O/ncu_interp.log 2>&1
 python tools/ncu_summary.py $O/prof_interp.ncu-rep --json $O/ncu_interp_summary.json > /dev/null 2>&1
 timeout 1200 python tools/table1.py --out $O/table1.md --json $O/table1.jsonl > $O/table1.log 2>&1
+rm -f $O/*.ncu-rep  # summaries kept; gpurun copies back <= 64 MiB
 echo done
