@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 
 struct aidw_ctx {
@@ -35,17 +36,44 @@ struct aidw_ctx {
     char err[512] = {0};
 };
 
+cudaError_t aidw::dev_malloc(void **p, size_t n)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        static std::mutex m;
+        static bool init[256] = {};
+        std::lock_guard<std::mutex> g(m);
+        if (dev >= 0 && dev < 256 && !init[dev]) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            init[dev] = true;
+        }
+    }
+    cudaError_t e = cudaMallocAsync(p, n, cudaStreamLegacy);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamLegacy);
+    return e;
+}
+
+void aidw::dev_free(void *p)
+{
+    if (p) cudaFreeAsync(p, cudaStreamLegacy);
+}
+
 void *aidw::SplitBuf::reserve(size_t n)
 {
     if (n <= bytes) return p;
     if (p) {
         cudaDeviceSynchronize();
-        cudaFree(p);
+        aidw::dev_free(p);
         p = nullptr;
         bytes = 0;
     }
     n = (n + (size_t(1) << 20) - 1) >> 20 << 20;
-    if (cudaMalloc(&p, n) != cudaSuccess) {
+    if (aidw::dev_malloc((void **)&p, n) != cudaSuccess) {
         cudaGetLastError();
         p = nullptr;
         return nullptr;
@@ -96,11 +124,11 @@ aidw_status ensure_work(aidw_t h, size_t bytes)
     if (h->work_bytes >= bytes) return AIDW_OK;
     if (h->work) {
         cudaDeviceSynchronize();
-        cudaFree(h->work);
+        aidw::dev_free(h->work);
         h->work = nullptr;
         h->work_bytes = 0;
     }
-    cudaError_t e = cudaMalloc(&h->work, bytes);
+    cudaError_t e = aidw::dev_malloc((void **)&h->work, bytes);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(h, AIDW_E_NOMEM, "cudaMalloc(%zu) for scratch: %s", bytes, cudaGetErrorString(e));
@@ -123,11 +151,11 @@ int *perm_for(aidw_t h, int64_t nq)
     if (h->perm_cap < nq) {
         if (h->perm) {
             cudaDeviceSynchronize();
-            cudaFree(h->perm);
+            aidw::dev_free(h->perm);
             h->perm = nullptr;
             h->perm_cap = 0;
         }
-        if (cudaMalloc(&h->perm, (size_t)nq * sizeof(int)) != cudaSuccess) {
+        if (aidw::dev_malloc((void **)&h->perm, (size_t)nq * sizeof(int)) != cudaSuccess) {
             cudaGetLastError();
             return nullptr;  // fall back to the unpermuted (general-formula) launch
         }
@@ -230,11 +258,11 @@ aidw_status aidw_create(aidw_t *out, int device, aidw_dtype dt, aidw_layout lay,
         return s;
     };
 
-    if ((e = cudaMalloc(&h->data, 3 * (size_t)h->ndp * ts)) != cudaSuccess) {
+    if ((e = aidw::dev_malloc((void **)&h->data, 3 * (size_t)h->ndp * ts)) != cudaSuccess) {
         cudaGetLastError();
         return bail(fail(h, AIDW_E_NOMEM, "cudaMalloc data: %s", cudaGetErrorString(e)));
     }
-    if ((e = cudaMalloc(&h->sc, sizeof(aidw::Scratch))) != cudaSuccess) {
+    if ((e = aidw::dev_malloc((void **)&h->sc, sizeof(aidw::Scratch))) != cudaSuccess) {
         cudaGetLastError();
         return bail(fail(h, AIDW_E_NOMEM, "cudaMalloc scratch: %s", cudaGetErrorString(e)));
     }
@@ -254,12 +282,12 @@ aidw_status aidw_create(aidw_t *out, int device, aidw_dtype dt, aidw_layout lay,
     const void *src = data_xyz;
     void *staged = nullptr;
     if (!is_device_ptr(data_xyz)) {  // host data: stage it
-        if ((e = cudaMalloc(&staged, in_bytes)) != cudaSuccess) {
+        if ((e = aidw::dev_malloc((void **)&staged, in_bytes)) != cudaSuccess) {
             cudaGetLastError();
             return bail(fail(h, AIDW_E_NOMEM, "cudaMalloc staging: %s", cudaGetErrorString(e)));
         }
         if ((e = cudaMemcpyAsync(staged, data_xyz, in_bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
-            cudaFree(staged);
+            aidw::dev_free(staged);
             return bail(cuda_fail(h, e, "H2D data"));
         }
         src = staged;
@@ -272,7 +300,7 @@ aidw_status aidw_create(aidw_t *out, int device, aidw_dtype dt, aidw_layout lay,
             (e = cudaStreamSynchronize(st)) != cudaSuccess)
             s = cuda_fail(h, e, "read bbox");
     }
-    if (staged) cudaFree(staged);
+    if (staged) aidw::dev_free(staged);
     if (s != AIDW_OK) return bail(s);
     if (back.nonfinite)
         return bail(fail(h, AIDW_E_NONFINITE_INPUT, "%llu data values are NaN/Inf", back.nonfinite));
@@ -302,10 +330,10 @@ aidw_status aidw_create(aidw_t *out, int device, aidw_dtype dt, aidw_layout lay,
         const double r1 = (rx + ry) * (1.0 + 1e-6);
         const bool safe = dt == AIDW_F32 || (std::isfinite(cxf) && std::isfinite(cyf) && r1 >= 0x1p-60 && r1 <= 0x1p60);
         if (!(env && env[0] == '0') && safe) {
-            if ((e = cudaMalloc(&h->filt.arrays, 8 * (size_t)h->ndp * sizeof(float))) != cudaSuccess ||
-                (e = cudaMalloc(&h->filt.cell_start, (aidw::kCells + 1) * sizeof(int))) != cudaSuccess ||
+            if ((e = aidw::dev_malloc((void **)&h->filt.arrays, 8 * (size_t)h->ndp * sizeof(float))) != cudaSuccess ||
+                (e = aidw::dev_malloc((void **)&h->filt.cell_start, (aidw::kCells + 1) * sizeof(int))) != cudaSuccess ||
                 (dt == AIDW_F64 &&
-                 (e = cudaMalloc(&h->filt.coords64, 2 * (size_t)h->ndp * sizeof(double))) != cudaSuccess)) {
+                 (e = aidw::dev_malloc((void **)&h->filt.coords64, 2 * (size_t)h->ndp * sizeof(double))) != cudaSuccess)) {
                 cudaGetLastError();
                 return bail(fail(h, AIDW_E_NOMEM, "cudaMalloc filter: %s", cudaGetErrorString(e)));
             }
@@ -743,15 +771,15 @@ aidw_status aidw_destroy(aidw_t h)
     cudaSetDevice(h->device);
     if (h->ex_own || h->ex_connected) aidw_exchange_close(h);
     if (h->data || h->sc || h->work || h->filt.arrays || h->perm || h->split.p) cudaDeviceSynchronize();
-    if (h->data) cudaFree(h->data);
-    if (h->sc) cudaFree(h->sc);
-    if (h->work) cudaFree(h->work);
-    if (h->filt.arrays) cudaFree(h->filt.arrays);
-    if (h->filt.cell_start) cudaFree(h->filt.cell_start);
-    if (h->filt.coords64) cudaFree(h->filt.coords64);
-    if (h->filt.qorder.p) cudaFree(h->filt.qorder.p);
-    if (h->perm) cudaFree(h->perm);
-    if (h->split.p) cudaFree(h->split.p);
+    if (h->data) aidw::dev_free(h->data);
+    if (h->sc) aidw::dev_free(h->sc);
+    if (h->work) aidw::dev_free(h->work);
+    if (h->filt.arrays) aidw::dev_free(h->filt.arrays);
+    if (h->filt.cell_start) aidw::dev_free(h->filt.cell_start);
+    if (h->filt.coords64) aidw::dev_free(h->filt.coords64);
+    if (h->filt.qorder.p) aidw::dev_free(h->filt.qorder.p);
+    if (h->perm) aidw::dev_free(h->perm);
+    if (h->split.p) aidw::dev_free(h->split.p);
     delete h;
     return AIDW_OK;
 }

@@ -30,6 +30,15 @@ __host__ __device__ inline int block_tile(int b, int ntiles, int nblk)
     return (int)((long long)b * ntiles / nblk);
 }
 
+// Device memory of handles and their scratch buffers: the device's default stream-ordered
+// pool with an unlimited release threshold, so a destroy + create cycle (a serving
+// process swapping data sets, bench.py e2e_full) reuses memory instead of paying
+// cudaFree / cudaMalloc.  dev_malloc returns memory usable from any stream at once;
+// callers synchronise the device before dev_free (as before with cudaFree).  The
+// exchange buffer keeps cudaMalloc (CUDA IPC needs it).
+cudaError_t dev_malloc(void **p, size_t n);
+void dev_free(void *p);
+
 // Growable device buffer for the small-nq data split (per-split kNN lists, per-block
 // weighting sums).  reserve() grows it (device sync + free + malloc) and returns
 // nullptr on allocation failure, in which case the launcher runs unsplit.
