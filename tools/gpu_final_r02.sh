@@ -2,7 +2,7 @@
 # build + smoke, pytest -m gpu (C4 + C5 golden), the default bench line, C5 strong N = 1,
 # a 2-rank gloo logic run of the default bench (ranks share the GPU), the reference
 # (oracle) arm, the ncu launch list of the bench step, ncu captures of the kNN and the
-# weighting kernel, the C4 strong-scaling shares, the Table-1 ablation.
+# weighting kernel, the C4 strong-scaling shares, every config per stage, the Table-1 ablation.
 cd "${GRAFT_REPO_ROOT:-.}"
 TAG=${1:-r02final}
 O=gpurun_out/$TAG
@@ -28,6 +28,8 @@ python tools/strong_shares.py $O/bench.json $O/share_512000.json $O/share_256000
     > $O/strong_shares.json 2>> $O/bench.err
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"interp_f32x2" -c 1 -o $O/prof_interp python bench.py --profile --warmup 0 > $O/ncu_interp.log 2>&1
 python tools/ncu_summary.py $O/prof_interp.ncu-rep --json $O/ncu_interp_summary.json > /dev/null 2>&1
+timeout 900 python tools/configs_bench.py --out $O/configs_f32.json > $O/configs.log 2>&1
+timeout 900 python tools/configs_bench.py --configs C1,C2,C3,C4 --dtypes f64 --out $O/configs_f64.json >> $O/configs.log 2>&1
 timeout 1200 python tools/table1.py --out $O/table1.md --json $O/table1.jsonl > $O/table1.log 2>&1
 rm -f $O/*.ncu-rep  # summaries kept; gpurun copies back <= 64 MiB
 echo done
