@@ -779,7 +779,11 @@ static int dispatch_filter_k(const KnnArgs<double> &a, const FilterArgs &f, cuda
         return launch_knn_filter_t<10, 2, 16, 0, double>(a, f, st, sp, fd);
     }
     if (k <= 12) return launch_knn_filter_t<12, 2, 16, 0, double>(a, f, st, sp, fd);
-    if (k <= 15) return launch_knn_filter_t<15, 2, 16, 0, double>(a, f, st, sp, fd);
+    if (k <= 15) {  // C3-like ordered batches: the fp16 stages as for k = 10
+        if (fd && fd->cell_start && order_queries(a.nq) && a.nq >= 32768 && knn_h16_mode() != 0)
+            return launch_knn_filter_t<15, 2, 32, 0, double, true>(a, f, st, sp, fd);
+        return launch_knn_filter_t<15, 2, 16, 0, double>(a, f, st, sp, fd);
+    }
     if (k <= 16) return launch_knn_filter_t<16, 2, 16, 0, double>(a, f, st, sp, fd);
     if (k <= 24) return launch_knn_filter_t<24, 1, 16, 0, double>(a, f, st, sp, fd);
     return launch_knn_filter_t<32, 1, 16, 0, double>(a, f, st, sp, fd);

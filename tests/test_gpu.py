@@ -772,8 +772,9 @@ def test_knn_filter_translated_scaled(P, orc, offset, scale):
     assert rel_err(Zg, Zo).max() <= 1e-4
 
 
-@pytest.mark.parametrize("case", ["uniform", "clustered", "offset", "scaled", "outliers"])
-def test_knn_h16_f64_bit_identical(P, orc, monkeypatch, case):
+@pytest.mark.parametrize("case,k", [("uniform", 10), ("clustered", 10), ("offset", 10), ("scaled", 10),
+                                    ("outliers", 10), ("clustered", 15), ("outliers", 15)])
+def test_knn_h16_f64_bit_identical(P, orc, monkeypatch, case, k):
     """fp64 handles with the fp16 pre-filter and strip test (round 2; the converted points
     are the centred fp32 filter coordinates, the centring rounding in the margin,
     passes.cuh H16Frame): on off-grid fp64 inputs -- uniform, clustered, translated by
@@ -801,12 +802,12 @@ def test_knn_h16_f64_bit_identical(P, orc, monkeypatch, case):
     for flag in ("0", "1"):
         monkeypatch.setenv("AIDW_KNN_H16", flag)
         eng = P.AIDW(x, y, z, dtype=torch.float64)
-        res[flag] = gpu_knn(P, eng, qx, qy, 10)
+        res[flag] = gpu_knn(P, eng, qx, qy, k)
         eng.close()
     for u, v in zip(res["0"], res["1"]):
         assert np.array_equal(u, v)
     sub = np.arange(0, nq, 197)
-    ro, do = orc.knn_f64(x, y, qx[sub], qy[sub], 10, want_dists=True)
+    ro, do = orc.knn_f64(x, y, qx[sub], qy[sub], k, want_dists=True)
     assert np.array_equal(res["1"][3][sub], do) and np.array_equal(res["1"][0][sub], ro)
 
 
@@ -844,3 +845,19 @@ def test_knn_filter_f64(P, orc, monkeypatch, offset, scale, nq):
     assert np.array_equal(res["1"][3][idx], do)
     assert np.array_equal(res["1"][0][idx], ro)
     assert np.array_equal(res["1"][1][idx], d1o)
+
+
+def test_handle_memory_reused(P):
+    """Handles take their device memory from the stream-ordered pool (aidw_api.cu
+    dev_malloc): repeated create / run / destroy cycles at one size reuse it -- the
+    device's free memory after the 10th cycle equals that after the 2nd (no leak)."""
+    x, y, z, qx, qy = datagen.random_cloud(808, 200000, 50000)
+    free = []
+    for i in range(10):
+        eng = P.AIDW(x, y, z)
+        eng.run(qx, qy, 10, LV, P.GLOBAL)
+        torch.cuda.synchronize()
+        eng.close()
+        torch.cuda.synchronize()
+        free.append(torch.cuda.mem_get_info()[0])
+    assert abs(free[-1] - free[1]) <= 64 * 2 ** 20, (free[1], free[-1])
