@@ -31,12 +31,16 @@
  *    bit-identical for any in-GPU split of the data range, query order or GPU count
  *    of the query-sharded path
  *    (DESIGN.md §4.6-4.7, §5).  The handle owns growable device scratch for the
- *    small-nq data split and the spatial query order (allocated on first use).
+ *    small-nq data split and the spatial query order (allocated on first use).  Handle
+ *    memory comes from the device's stream-ordered pool (cudaMallocAsync, kept on
+ *    destroy), so destroying and creating handles reuses it.
  *  - Tuning/testing environment variables (defaults are the measured best):
  *    AIDW_SPLIT=0|n (data split off / forced factor), AIDW_KNN_ORDER=0 (no
- *    spatial query order), AIDW_KNN_H16=0|1|2 (fp16 kNN pre-filter off / default /
- *    uncapped registers) and AIDW_EXP2_CLAMP=1 (always-clamped polynomial exp2) are read
- *    per call -- none changes a result; AIDW_ALPHA_CLASSES=0 (no
+ *    spatial query order), AIDW_KNN_H16=0|1|2|3 (fp16 kNN pre-filter off / default /
+ *    Q = 4 / register-capped shapes), AIDW_KNN_STRIP=0 (fp16 kernels without the strip
+ *    pre-test), AIDW_KNN_QSEED=0 (home-tile seeds instead of per-query seeds) and
+ *    AIDW_EXP2_CLAMP=1 (always-clamped polynomial exp2) are read per call -- none
+ *    changes a result; AIDW_ALPHA_CLASSES=0 (no
  *    exact-exponent weighting classes) and AIDW_KNN_VARIANT / AIDW_INTERP_VARIANT
  *    (tuning sweeps) once per process; AIDW_KNN_FILTER=0 (canonical kNN, no fp32
  *    filter, for either dtype) at aidw_create.  Spatially ordered kNN batches
