@@ -6,6 +6,7 @@
 #                                            at grids of 32.0 .. 48.05 waves)
 #   bash tools/gpu_sweeps.sh ncu_interp TAG  ncu --set full of the weighting kernel + its
 #                                            SASS source page (stall samples per instruction)
+#   bash tools/gpu_sweeps.sh ncu_knn TAG     the same for the kNN kernel
 cd "${GRAFT_REPO_ROOT:-.}"
 MODE=${1:?mode}
 O=gpurun_out/${2:-$MODE}; mkdir -p $O
@@ -40,5 +41,12 @@ ncu_interp)
       python bench.py --profile --warmup 0 > $O/ncu.log 2>&1
   ncu -i $O/prof_interp.ncu-rep --page source --csv --print-source sass > $O/source_sass.csv 2>/dev/null
   ;;
+ncu_knn)
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"knn_filter" -c 1 -o $O/prof_knn \
+      python bench.py --profile --warmup 0 > $O/ncu.log 2>&1
+  ncu -i $O/prof_knn.ncu-rep --page source --csv --print-source sass > $O/source_sass.csv 2>/dev/null
+  rm -f $O/prof_knn.ncu-rep
+  ;;
 esac
+rm -f $O/*.ncu-rep
 echo done
