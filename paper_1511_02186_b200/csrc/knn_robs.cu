@@ -151,7 +151,7 @@ __device__ __forceinline__ void warp_minmax(double v, bool valid, unsigned long 
 
 // Query loads for the Q queries of this thread (strided by the block for coalescing),
 // with the non-finite check (smallest failing index -> scratch).
-template <typename T, int Q>
+template <typename T, int Q, int BLK = kBlock>
 __device__ __forceinline__ void load_queries(const KnnArgs<T> &a, int64_t base, T (&qx)[Q], T (&qy)[Q],
                                              bool (&valid)[Q], int64_t (&qid)[Q])
 {
@@ -159,8 +159,8 @@ __device__ __forceinline__ void load_queries(const KnnArgs<T> &a, int64_t base, 
     Scratch *sc = a.sc;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        valid[q] = base + q * kBlock < a.nq;
-        const int64_t idx = qid[q] = query_of(a, base + q * kBlock);
+        valid[q] = base + q * BLK < a.nq;
+        const int64_t idx = qid[q] = query_of(a, base + q * BLK);
         qx[q] = valid[q] ? qxp[idx] : T(0);
         qy[q] = valid[q] ? qyp[idx] : T(0);
         if (valid[q] && !(isfinite(qx[q]) && isfinite(qy[q]))) atomicMin(&sc->err_idx, (long long)idx);
@@ -321,8 +321,8 @@ template <typename T> __host__ __device__ constexpr int filter_arrays() { return
 // (after the seed tile, or the first tile).  fp32 handles convert the tile's coordinates;
 // fp64 handles (round 2) convert the centred fp32 filter coordinates cx = fl32(x - c), the
 // CTA centre taken on the same centred scale, with the centring error in the margin.
-template <typename T, int K, int Q, int G, int SPLIT, int MINB = 0, bool H16 = false>
-__global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<T> a, const FilterArgs f)
+template <typename T, int K, int Q, int G, int SPLIT, int MINB = 0, bool H16 = false, int BLK = kBlock>
+__global__ void __launch_bounds__(BLK, MINB) knn_filter_kernel(const KnnArgs<T> a, const FilterArgs f)
 {
     constexpr int TILE = kTileKF, STAGES = kStagesKF, NARR = filter_arrays<T>();
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
     float *spp = scy + STAGES * TILE;
     float *spx = spp + STAGES * TILE;  // fp32 only
     float *spy = spx + STAGES * TILE;
-    Ring<STAGES> ring{reinterpret_cast<uint64_t *>(scx + NARR * STAGES * TILE),
+    Ring<STAGES, BLK / 32> ring{reinterpret_cast<uint64_t *>(scx + NARR * STAGES * TILE),
                       reinterpret_cast<uint64_t *>(scx + NARR * STAGES * TILE) + STAGES};
     const int nt_all = (int)(a.ndp / TILE);
     const TileRange tr = SPLIT ? split_range(nt_all) : TileRange{0, nt_all};
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
     // equals the seed value.
     int home = 0;
     if (a.perm) {
-        const int64_t mid = min((int64_t)blockIdx.x * (kBlock * Q) + kBlock * Q / 2, a.nq - 1);
+        const int64_t mid = min((int64_t)blockIdx.x * (BLK * Q) + BLK * Q / 2, a.nq - 1);
         const int64_t qm = a.perm[mid];
         home = (int)(f.cell_start[morton_cell((float)a.qx[qm], (float)a.qy[qm], f.grid)] / TILE);
         home = home >= nt_all ? nt_all - 1 : home;
@@ -382,11 +382,11 @@ __global__ void __launch_bounds__(kBlock, MINB) knn_filter_kernel(const KnnArgs<
     if (threadIdx.x == 0)
         for (int s = 0; s < STAGES && s < ntiles; ++s) issue(s, s);
 
-    const int64_t base = (int64_t)blockIdx.x * (kBlock * Q) + threadIdx.x;
+    const int64_t base = (int64_t)blockIdx.x * (BLK * Q) + threadIdx.x;
     T qx[Q], qy[Q];
     bool valid[Q];
     int64_t qid[Q];
-    load_queries<T, Q>(a, base, qx, qy, valid, qid);
+    load_queries<T, Q, BLK>(a, base, qx, qy, valid, qid);
     const int k0 = K - a.k;
     KnnF32State<K, Q, T> st;
 #pragma unroll
@@ -578,7 +578,8 @@ static int knn_split_factor(const void *kern, size_t smem, unsigned grid, int nt
 // (C4: 2,000 CTAs on 592 slots -> S = 5, 17 waves of 1/5 instead of 4 of 1).
 // AIDW_SPLIT=0 disables, AIDW_SPLIT=n forces n (tests).
 template <typename T>
-static int ordered_split_factor(const void *kern, size_t smem, unsigned grid, int ntiles, KnnArgs<T> &a, SplitBuf *sp)
+static int ordered_split_factor(const void *kern, size_t smem, unsigned grid, int ntiles, KnnArgs<T> &a, SplitBuf *sp,
+                                int blk = kBlock)
 {
     a.lists = nullptr;
     if (!sp) return 1;
@@ -592,7 +593,7 @@ static int ordered_split_factor(const void *kern, size_t smem, unsigned grid, in
         int dev = 0, sms = 148, occ = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, smem) != cudaSuccess) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, blk, smem) != cudaSuccess) {
             cudaGetLastError();
             return 1;
         }
@@ -624,9 +625,10 @@ template <typename T> static int knn_finish(const KnnArgs<T> &a, int S, cudaStre
 }
 
 // ---------------------------------------------------------------------------------
-template <typename T, int K, int Q, int G, int SPLIT, int MINB, bool H16 = false> static int set_filter_attrs(size_t smem)
+template <typename T, int K, int Q, int G, int SPLIT, int MINB, bool H16 = false, int BLK = kBlock>
+static int set_filter_attrs(size_t smem)
 {
-    auto kern = knn_filter_kernel<T, K, Q, G, SPLIT, MINB, H16>;
+    auto kern = knn_filter_kernel<T, K, Q, G, SPLIT, MINB, H16, BLK>;
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
                    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) == cudaSuccess
                ? 0
@@ -678,22 +680,23 @@ static int knn_h16_mode()
     return e ? atoi(e) : 1;
 }
 
-template <int K, int Q, int G = 8, int MINB = 0, typename T = float, bool H16 = false>
+template <int K, int Q, int G = 8, int MINB = 0, typename T = float, bool H16 = false, int BLK = kBlock>
 static int launch_knn_filter_t(KnnArgs<T> a, const FilterArgs &f, cudaStream_t st, SplitBuf *sp,
                                FilterData *fd)
 {
     const size_t smem =
         (size_t)filter_arrays<T>() * kStagesKF * kTileKF * sizeof(float) + 2 * kStagesKF * sizeof(uint64_t);
     if (set_filter_attrs<T, K, Q, G, 0, MINB>(smem) < 0) return -1;
-    const int64_t per_cta = (int64_t)kBlock * Q;
-    const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
     // A spatially ordered batch splits only with seeded lists (knn_filter_kernel), by the
     // factor that best fills the last wave (ordered_split_factor); an unordered one by
     // whole extra waves (knn_split_factor: its splits restart the top-k warm-up).
     const bool ordered = fd && fd->cell_start && order_queries(a.nq);
-    if (ordered && set_filter_attrs<T, K, Q, G, 1, MINB, H16>(smem) < 0) return -1;
-    const int S = ordered ? ordered_split_factor((const void *)knn_filter_kernel<T, K, Q, G, 1, MINB, H16>, smem,
-                                                 grid, (int)(a.ndp / kTileKF), a, sp)
+    const int blk = (H16 && ordered) ? BLK : kBlock;  // BLK: the fp16 kernels' CTA size
+    const int64_t per_cta = (int64_t)blk * Q;
+    const unsigned grid = (unsigned)((a.nq + per_cta - 1) / per_cta);
+    if (ordered && set_filter_attrs<T, K, Q, G, 1, MINB, H16, (H16 ? BLK : kBlock)>(smem) < 0) return -1;
+    const int S = ordered ? ordered_split_factor((const void *)knn_filter_kernel<T, K, Q, G, 1, MINB, H16, (H16 ? BLK : kBlock)>,
+                                                 smem, grid, (int)(a.ndp / kTileKF), a, sp, blk)
                           : knn_split_factor((const void *)knn_filter_kernel<T, K, Q, G, 0, MINB>, smem, grid,
                                              (int)(a.ndp / kTileKF), a, sp);
     int pre = 0;
@@ -725,8 +728,8 @@ static int launch_knn_filter_t(KnnArgs<T> a, const FilterArgs &f, cudaStream_t s
     }
     if (S == 1) {
         if (H16 && ordered) {
-            if (set_filter_attrs<T, K, Q, G, 0, MINB, H16>(smem) < 0) return -1;
-            knn_filter_kernel<T, K, Q, G, 0, MINB, H16><<<grid, kBlock, smem, st>>>(a, fo);
+            if (set_filter_attrs<T, K, Q, G, 0, MINB, H16, BLK>(smem) < 0) return -1;
+            knn_filter_kernel<T, K, Q, G, 0, MINB, H16, BLK><<<grid, BLK, smem, st>>>(a, fo);
         } else {
             knn_filter_kernel<T, K, Q, G, 0, MINB><<<grid, kBlock, smem, st>>>(a, fo);
         }
@@ -742,8 +745,8 @@ static int launch_knn_filter_t(KnnArgs<T> a, const FilterArgs &f, cudaStream_t s
             }
         }
         if (ordered) {
-            if (set_filter_attrs<T, K, Q, G, 1, MINB, H16>(smem) < 0) return -1;
-            knn_filter_kernel<T, K, Q, G, 1, MINB, H16><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, fo);
+            if (set_filter_attrs<T, K, Q, G, 1, MINB, H16, (H16 ? BLK : kBlock)>(smem) < 0) return -1;
+            knn_filter_kernel<T, K, Q, G, 1, MINB, H16, (H16 ? BLK : kBlock)><<<dim3(grid, (unsigned)S), blk, smem, st>>>(a, fo);
         } else {
             if (set_filter_attrs<T, K, Q, G, 2, MINB>(smem) < 0) return -1;
             knn_filter_kernel<T, K, Q, G, 2, MINB><<<dim3(grid, (unsigned)S), kBlock, smem, st>>>(a, fo);
@@ -817,6 +820,7 @@ static int dispatch_filter_k(const KnnArgs<float> &a, const FilterArgs &f, cudaS
         case 29: return launch_knn_filter_t<10, 4, 32, 5, float, true>(a, f, st, sp, fd);  // fp16, Q = 4, 5 CTAs/SM
         case 30: return launch_knn_filter_t<10, 2, 32, 7, float, true>(a, f, st, sp, fd);  // fp16, Q = 2, 7 CTAs/SM
         case 31: return launch_knn_filter_t<10, 4, 32, 3, float, true>(a, f, st, sp, fd);  // fp16, Q = 4, 3 CTAs/SM
+        case 32: return launch_knn_filter_t<10, 2, 32, 0, float, true, 256>(a, f, st, sp, fd);  // fp16, 256-thread CTAs
         default: break;
         }
     }
