@@ -443,11 +443,11 @@ __device__ __forceinline__ void h16_convert(const float *__restrict__ tpx, const
 }
 
 // The fp16 main loop over one tile (same groups, votes and rare path as knn_f32_tile).
-// STRIP (round 2, DESIGN.md §4.1 "strip pre-test"): every group of G points is first
-// tested on ONE axis (the first, h16_convert), t̂1 = p̂s + Â û (one HFMA2 per couple instead
-// of two: 1.6x the pairs per clock, tools/knn_loop_bench.cu); only a group that some
-// lane's strip test keeps runs the 2-D test, and only a group that passes both reaches
-// the rare path.  Both tests are necessary conditions of a true candidate, so the
+// STRIP (round 2, DESIGN.md §4.1 "strip pre-test"): every strip group of SGM * G points is
+// first tested on ONE axis (the first, h16_convert), t̂1 = p̂s + Â û (one HFMA2 per couple
+// instead of two: 1.6x the pairs per clock, tools/knn_loop_bench.cu) under one warp vote;
+// a kept strip group runs the 2-D test per G-point group, and only a group that passes both
+// reaches the rare path.  Both tests are necessary conditions of a true candidate, so the
 // selected multiset is unchanged.  !STRIP: the 2-D test alone (AIDW_KNN_STRIP=0).
 template <int K, int Q, int G, int TILE, bool STRIP, int SGM = 1, typename T = float>
 __device__ __forceinline__ void knn_h16_tile(KnnF32State<K, Q, T> &st, KnnH16<Q> &h, const __half2 *hu,
