@@ -419,26 +419,28 @@ __device__ __forceinline__ void h16_convert(const float *__restrict__ tpx, const
                                             __half2 *__restrict__ hp, __half2 *__restrict__ hs, int axis,
                                             float Cx, float Cy, float sig)
 {
+    const f32x2 C2x = splat2(Cx), C2y = splat2(Cy), S2 = splat2(sig);
     for (int i = threadIdx.x; i < TILE / 2; i += blockDim.x) {
-        const float2 x = *reinterpret_cast<const float2 *>(tpx + 2 * i);
-        const float2 y = *reinterpret_cast<const float2 *>(tpy + 2 * i);
-        const float u0 = fminf(fmaxf(__fmul_rn(__fsub_rn(x.x, Cx), sig), -kH16Clamp), kH16Clamp);
-        const float u1 = fminf(fmaxf(__fmul_rn(__fsub_rn(x.y, Cx), sig), -kH16Clamp), kH16Clamp);
-        const float v0 = fminf(fmaxf(__fmul_rn(__fsub_rn(y.x, Cy), sig), -kH16Clamp), kH16Clamp);
-        const float v1 = fminf(fmaxf(__fmul_rn(__fsub_rn(y.y, Cy), sig), -kH16Clamp), kH16Clamp);
+        // packed fp32x2 arithmetic: each lane is the IEEE round-to-nearest scalar op
+        const f32x2 x = mul2(sub2(*reinterpret_cast<const f32x2 *>(tpx + 2 * i), C2x), S2);
+        const f32x2 y = mul2(sub2(*reinterpret_cast<const f32x2 *>(tpy + 2 * i), C2y), S2);
+        const float u0 = fminf(fmaxf(x.x, -kH16Clamp), kH16Clamp);
+        const float u1 = fminf(fmaxf(x.y, -kH16Clamp), kH16Clamp);
+        const float v0 = fminf(fmaxf(y.x, -kH16Clamp), kH16Clamp);
+        const float v1 = fminf(fmaxf(y.y, -kH16Clamp), kH16Clamp);
         __half2 U = __floats2half2_rn(u0, u1), V = __floats2half2_rn(v0, v1);
         if (axis == 1) {  // the strip axis always goes first (the coefficients are swapped too)
             const __half2 w = U;
             U = V;
             V = w;
         }
-        const float2 uf = __half22float2(U), vf = __half22float2(V);
-        const float p0 = fminf(__fmaf_rn(uf.x, uf.x, __fmul_rn(vf.x, vf.x)), kH16PPClamp);
-        const float p1 = fminf(__fmaf_rn(uf.y, uf.y, __fmul_rn(vf.y, vf.y)), kH16PPClamp);
+        const f32x2 uf = __half22float2(U), vf = __half22float2(V);
+        const f32x2 p = fma2(uf, uf, mul2(vf, vf));  // û² + v̂², exact (11-bit operands)
+        const f32x2 q = mul2(uf, uf);                // û², exact
         hu[i] = U;
         hv[i] = V;
-        hp[i] = __floats2half2_rn(p0, p1);
-        hs[i] = __floats2half2_rn(fminf(__fmul_rn(uf.x, uf.x), kH16PPClamp), fminf(__fmul_rn(uf.y, uf.y), kH16PPClamp));
+        hp[i] = __floats2half2_rn(fminf(p.x, kH16PPClamp), fminf(p.y, kH16PPClamp));
+        hs[i] = __floats2half2_rn(fminf(q.x, kH16PPClamp), fminf(q.y, kH16PPClamp));
     }
 }
 
