@@ -420,15 +420,16 @@ __device__ __forceinline__ void h16_convert(const float *__restrict__ tpx, const
                                             float Cx, float Cy, float sig)
 {
     const f32x2 C2x = splat2(Cx), C2y = splat2(Cy), S2 = splat2(sig);
-    for (int i = threadIdx.x; i < TILE / 2; i += blockDim.x) {
+    auto couple = [&](f32x2 xr, f32x2 yr, __half2 &U, __half2 &V, __half2 &Pp, __half2 &Ps) {
         // packed fp32x2 arithmetic: each lane is the IEEE round-to-nearest scalar op
-        const f32x2 x = mul2(sub2(*reinterpret_cast<const f32x2 *>(tpx + 2 * i), C2x), S2);
-        const f32x2 y = mul2(sub2(*reinterpret_cast<const f32x2 *>(tpy + 2 * i), C2y), S2);
+        const f32x2 x = mul2(sub2(xr, C2x), S2);
+        const f32x2 y = mul2(sub2(yr, C2y), S2);
         const float u0 = fminf(fmaxf(x.x, -kH16Clamp), kH16Clamp);
         const float u1 = fminf(fmaxf(x.y, -kH16Clamp), kH16Clamp);
         const float v0 = fminf(fmaxf(y.x, -kH16Clamp), kH16Clamp);
         const float v1 = fminf(fmaxf(y.y, -kH16Clamp), kH16Clamp);
-        __half2 U = __floats2half2_rn(u0, u1), V = __floats2half2_rn(v0, v1);
+        U = __floats2half2_rn(u0, u1);
+        V = __floats2half2_rn(v0, v1);
         if (axis == 1) {  // the strip axis always goes first (the coefficients are swapped too)
             const __half2 w = U;
             U = V;
@@ -437,10 +438,20 @@ __device__ __forceinline__ void h16_convert(const float *__restrict__ tpx, const
         const f32x2 uf = __half22float2(U), vf = __half22float2(V);
         const f32x2 p = fma2(uf, uf, mul2(vf, vf));  // û² + v̂², exact (11-bit operands)
         const f32x2 q = mul2(uf, uf);                // û², exact
-        hu[i] = U;
-        hv[i] = V;
-        hp[i] = __floats2half2_rn(fminf(p.x, kH16PPClamp), fminf(p.y, kH16PPClamp));
-        hs[i] = __floats2half2_rn(fminf(q.x, kH16PPClamp), fminf(q.y, kH16PPClamp));
+        Pp = __floats2half2_rn(fminf(p.x, kH16PPClamp), fminf(p.y, kH16PPClamp));
+        Ps = __floats2half2_rn(fminf(q.x, kH16PPClamp), fminf(q.y, kH16PPClamp));
+    };
+    // four points per thread per pass: one LDS.128 per coordinate, 8-byte stores
+    for (int i = threadIdx.x; i < TILE / 4; i += blockDim.x) {
+        const float4 X = *reinterpret_cast<const float4 *>(tpx + 4 * i);
+        const float4 Y = *reinterpret_cast<const float4 *>(tpy + 4 * i);
+        __half2 U[2], V[2], Pp[2], Ps[2];
+        couple(pack2(X.x, X.y), pack2(Y.x, Y.y), U[0], V[0], Pp[0], Ps[0]);
+        couple(pack2(X.z, X.w), pack2(Y.z, Y.w), U[1], V[1], Pp[1], Ps[1]);
+        *reinterpret_cast<uint2 *>(hu + 2 * i) = *reinterpret_cast<const uint2 *>(U);
+        *reinterpret_cast<uint2 *>(hv + 2 * i) = *reinterpret_cast<const uint2 *>(V);
+        *reinterpret_cast<uint2 *>(hp + 2 * i) = *reinterpret_cast<const uint2 *>(Pp);
+        *reinterpret_cast<uint2 *>(hs + 2 * i) = *reinterpret_cast<const uint2 *>(Ps);
     }
 }
 
