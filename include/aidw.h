@@ -38,7 +38,8 @@
  *    AIDW_SPLIT=0|n (data split off / forced factor), AIDW_KNN_ORDER=0 (no
  *    spatial query order), AIDW_KNN_H16=0|1|2|3 (fp16 kNN pre-filter off / default /
  *    Q = 4 / register-capped shapes), AIDW_KNN_STRIP=0 (fp16 kernels without the strip
- *    pre-test), AIDW_KNN_QSEED=0 (home-tile seeds instead of per-query seeds) and
+ *    pre-test), AIDW_KNN_PIPE=0 (fp16 tiles behind a CTA barrier instead of the
+ *    mbarrier pipeline), AIDW_KNN_QSEED=0 (home-tile seeds instead of per-query seeds) and
  *    AIDW_EXP2_CLAMP=1 (always-clamped polynomial exp2) are read per call -- none
  *    changes a result; AIDW_ALPHA_CLASSES=0 (no
  *    exact-exponent weighting classes) and AIDW_KNN_VARIANT / AIDW_INTERP_VARIANT

@@ -408,7 +408,9 @@ __global__ void __launch_bounds__(BLK, MINB) knn_filter_kernel(const KnnArgs<T> 
 
     // fp16 pre-filter state (H16): the CTA's query-bbox centre, the scale, per-query
     // coefficients and thresholds; enabled once every query has a finite k-th distance
-    __shared__ __align__(16) __half2 hbuf[H16 ? 2 : 1][4][H16 ? TILE / 2 : 1];
+    __shared__ __align__(16) __half2 hbuf[H16 ? 3 : 1][4][H16 ? TILE / 2 : 1];
+    __shared__ __align__(8) uint64_t hbar[H16 ? 6 : 1];  // pipelined fp16 tiles: full[3], empty[3]
+    __shared__ unsigned hrel[H16 ? STAGES : 1];          // pipelined: warps done with each ring slot
     __shared__ unsigned hred[4];
     __shared__ H16Frame hfr;
     KnnH16<Q> h16;
@@ -494,7 +496,72 @@ __global__ void __launch_bounds__(BLK, MINB) knn_filter_kernel(const KnnArgs<T> 
         if (qseed) h16_on = h16_enable();  // seeded lists: fp16 from the first tile
     }
 
-    for (int t = 0; t < ntiles; ++t) {
+    // Pipelined fp16 tiles (round 2): with the fp16 stages on from the first
+    // tile (per-query seeds) and the strip test, every warp converts its quarter of tile t+1
+    // into one of three fp16 buffers before it processes tile t, and hands the buffers over
+    // with mbarriers (full: all four quarters written; empty: all four warps done reading)
+    // instead of a CTA barrier per tile -- a warp may run a tile ahead of the slowest one.
+    // The converted values and the per-tile work are the same: results bit-identical.
+    bool piped = false;
+    if constexpr (H16) {
+        piped = h16_on && axis >= 0 && f.pipe != 0;
+        if (piped) {
+            if (threadIdx.x == 0) {
+                for (int b = 0; b < 6; ++b) mbar_init(&hbar[b], BLK);  // every thread arrives
+                for (int b = 0; b < STAGES; ++b) hrel[b] = 0u;
+                fence_mbar_init();
+            }
+            __syncthreads();
+            auto convert = [&](int t) {  // this thread's 4 points of tile t -> buffer t % 3
+                const int o = ring.slot(t) * TILE;
+                __half2 *hb = &hbuf[t % 3][0][0];
+                h16_convert<TILE>(NARR == 5 ? spx + o : scx + o, NARR == 5 ? spy + o : scy + o, hb, hb + TILE / 2,
+                                  hb + TILE, hb + 3 * TILE / 2, axis, Cx, Cy, sig);
+                mbar_arrive(&hbar[t % 3]);  // release: this thread's stores
+            };
+            ring.wait_full(0);
+            convert(0);
+            for (int t = 0; t < ntiles; ++t) {
+                if (t + 1 < ntiles) {
+                    ring.wait_full(t + 1);
+                    if (t >= 2) mbar_wait(&hbar[3 + (t + 1) % 3], (uint32_t)((t - 2) / 3) & 1u);  // tile t-2 read
+                    convert(t + 1);
+                }
+                mbar_wait(&hbar[t % 3], (uint32_t)(t / 3) & 1u);  // tile t converted by every warp
+                const int o = ring.slot(t) * TILE;
+                __half2 *hb = &hbuf[t % 3][0][0];
+                const T *rpx, *rpy;
+                if constexpr (NARR == 5) {
+                    rpx = spx + o;
+                    rpy = spy + o;
+                } else {
+                    const int64_t off = (int64_t)tile_of(t) * TILE;
+                    rpx = f.px64 + off;
+                    rpy = f.py64 + off;
+                }
+                knn_h16_tile<K, Q, G, TILE, true, 4, T>(st, h16, hb, hb + TILE / 2, hb + TILE, hb + 3 * TILE / 2,
+                                                        scx + o, scy + o, spp + o, rpx, rpy, hfr);
+                mbar_arrive(&hbar[3 + t % 3]);  // this thread has read buffer t % 3
+                // the LAST warp to finish tile t refills its ring slot (no warp waits for the
+                // others here; the slot's reads are ordered before the TMA write by the
+                // acq_rel counter and the async-proxy fence)
+                __syncwarp();
+                if ((threadIdx.x & 31) == 0 && t + STAGES < ntiles) {
+                    const int sl = ring.slot(t);
+                    unsigned old;
+                    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                                 : "=r"(old) : "r"(smem_u32(&hrel[sl])) : "memory");
+                    if (old == BLK / 32 - 1) {
+                        hrel[sl] = 0u;
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        issue(t + STAGES, sl);
+                    }
+                }
+            }
+        }
+    }
+
+    for (int t = 0; t < (piped ? 0 : ntiles); ++t) {
         ring.wait_full(t);
         const int o = ring.slot(t) * TILE;
         if constexpr (H16) {
@@ -665,6 +732,14 @@ static bool knn_qseed_enabled()
     return !(e && e[0] == '0');
 }
 
+// AIDW_KNN_PIPE=0: the fp16 kernels convert each tile behind a CTA barrier (no mbarrier
+// hand-off between warps).
+static int knn_pipe_env()
+{
+    const char *e = getenv("AIDW_KNN_PIPE");
+    return (e && e[0] == '0') ? 0 : 1;
+}
+
 // AIDW_KNN_STRIP=0: the fp16 kernels run the 2-D test on every group (no strip pre-test).
 static int knn_strip_enabled()
 {
@@ -702,6 +777,7 @@ static int launch_knn_filter_t(KnnArgs<T> a, const FilterArgs &f, cudaStream_t s
     int pre = 0;
     FilterArgs fo = f;
     fo.strip = knn_strip_enabled();
+    fo.pipe = knn_pipe_env();
     if (ordered) {
         pre = launch_order_queries(a.qx, a.qy, a.nq, fd, &fd->qorder, &a.perm, st);
         if (pre < 0) return -1;

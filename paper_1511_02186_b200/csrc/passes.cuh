@@ -102,6 +102,7 @@ struct FilterArgs {
     const float *sx = nullptr, *sy = nullptr;
     const double *sx64 = nullptr, *sy64 = nullptr;
     int strip = 1;  // fp16 kernels: 1 = strip pre-test, 0 = the 2-D test only
+    int pipe = 1;   // fp16 kernels: 1 = mbarrier-pipelined fp16 tiles, 0 = a CTA barrier per tile
 };
 
 // thr_of: the filter threshold for the canonical k-th distance thr, in fp32 with every
